@@ -1,0 +1,189 @@
+/*
+ * qrtebd_c.h — C-ABI of the B200-native QR-TEBD bond update.
+ *
+ * This is the drop-in boundary for the hot path named in BASELINE.json:
+ * the two-site QR/QR+CBE update of arXiv 2212.09782 and the observables that
+ * read its output.  Every entry point replaces one function of the reference
+ * C++ library (/root/reference/proj, cited as file:line below); the C++
+ * mirror in include/qrtebd/qrtebd.hpp re-exposes them under the reference's
+ * own names and types.
+ *
+ * Conventions (reference proj/include/qrtebd/tensor.hpp:14-61):
+ *   - tensors are dense, row-major (last axis fastest), interleaved
+ *     complex128: element k occupies doubles [2k, 2k+1] = (re, im);
+ *   - site tensors are (d, chi_left, chi_right); bond matrices chi x chi;
+ *     gates are (i_out, j_out, i_in, j_in) (gates.hpp:16-23);
+ *   - qt_tensor handles live in device memory (HBM) and are owned by the
+ *     caller; outputs are freshly allocated handles, inputs are never
+ *     mutated (value semantics);
+ *   - all work on a context is ordered on that context's CUDA stream; a
+ *     context must not be used from two host threads at once;
+ *   - errors map onto the reference taxonomy (errors.hpp:9-30):
+ *     ShapeError -> QT_ERR_SHAPE, InputError -> QT_ERR_INPUT,
+ *     NumericError -> QT_ERR_NUMERIC, CapacityError -> QT_ERR_CAPACITY;
+ *     qt_last_error() returns the thread-local message of the last failure.
+ *
+ * There is no CPU fallback: every compute entry point runs sm_100a kernels
+ * and fails with QT_ERR_CUDA when no suitable device is present.
+ */
+#ifndef QRTEBD_C_H
+#define QRTEBD_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum qt_status {
+  QT_OK = 0,
+  QT_ERR_SHAPE = 1,
+  QT_ERR_INPUT = 2,
+  QT_ERR_NUMERIC = 3,
+  QT_ERR_CAPACITY = 4,
+  QT_ERR_CUDA = 5,
+  QT_ERR_NCCL = 6,
+  QT_ERR_INTERNAL = 7
+} qt_status;
+
+/* Scheme, proj/include/qrtebd/gates.hpp:30.  Only QR and QR_CBE run on the
+ * device; SVD/EIG are the CPU comparators of the reference and are rejected
+ * with QT_ERR_INPUT. */
+typedef enum qt_scheme { QT_SCHEME_SVD = 0, QT_SCHEME_EIG = 1, QT_SCHEME_QR = 2, QT_SCHEME_QR_CBE = 3 } qt_scheme;
+
+/* TruncationPolicy, proj/include/qrtebd/gates.hpp:43-55 (same fields, same
+ * defaults via qt_policy_default). */
+typedef struct qt_policy {
+  uint64_t chi_max;            /* 1024 */
+  double sv_cutoff;            /* 1e-14 */
+  double target_eps;           /* 0 */
+  uint64_t delta_chi_abs;      /* 100 */
+  double delta_chi_rel;        /* 0.1 */
+  uint64_t chi_max_expansion;  /* 0 = no cap */
+  int32_t qr_sweeps;           /* 1 */
+  int32_t compute_explicit_error; /* 1 */
+  int32_t skip_renormalize;    /* 0 */
+  int32_t reserved;
+} qt_policy;
+
+/* TruncationReport, proj/include/qrtebd/gates.hpp:57-64. */
+typedef struct qt_report {
+  uint64_t chi_before;
+  uint64_t chi_expanded;
+  uint64_t chi_after;
+  double eps_trunc;
+  double discarded_weight;
+  int32_t scheme;
+  int32_t reserved;
+} qt_report;
+
+/* BondReport, proj/include/qrtebd/gates.hpp:106-109. */
+typedef struct qt_bond_report {
+  uint64_t bond;
+  qt_report report;
+} qt_bond_report;
+
+typedef struct qt_ctx qt_ctx;
+typedef struct qt_tensor qt_tensor;
+
+/* ---- library ------------------------------------------------------------ */
+const char* qt_last_error(void);
+const char* qt_version(void);
+/* TruncationPolicy{} defaults, gates.hpp:44-53. */
+void qt_policy_default(qt_policy* p);
+/* TruncationPolicy::expanded_dim, proj/src/gates.cpp:94-101. */
+uint64_t qt_expanded_dim(const qt_policy* p, uint64_t chi, uint64_t d);
+/* number of device kernels this library has launched (bench bookkeeping) */
+uint64_t qt_kernel_launches(void);
+
+/* ---- context ------------------------------------------------------------ */
+/* stream == NULL: the context creates and owns a non-blocking stream. */
+qt_status qt_ctx_create(int device, void* stream, qt_ctx** out);
+qt_status qt_ctx_destroy(qt_ctx* ctx);
+qt_status qt_ctx_synchronize(qt_ctx* ctx);
+void* qt_ctx_stream(qt_ctx* ctx);
+
+/* ---- device tensors (ComplexTensor, tensor.hpp:18-61) --------------------- */
+qt_status qt_tensor_create(qt_ctx* ctx, int rank, const uint64_t* shape, qt_tensor** out);
+/* non-owning view of caller device memory (interleaved complex128) */
+qt_status qt_tensor_wrap(qt_ctx* ctx, int rank, const uint64_t* shape, void* device_ptr, qt_tensor** out);
+qt_status qt_tensor_free(qt_tensor* t);
+/* shape4 receives up to 4 extents; *rank the number of axes */
+qt_status qt_tensor_shape(const qt_tensor* t, int* rank, uint64_t* shape4);
+void* qt_tensor_data(const qt_tensor* t);
+/* synchronous host<->device copies of 2*numel doubles */
+qt_status qt_tensor_upload(qt_tensor* t, const double* host);
+qt_status qt_tensor_download(const qt_tensor* t, double* host);
+/* asynchronous variants (host memory should be pinned) */
+qt_status qt_tensor_upload_async(qt_tensor* t, const double* host);
+qt_status qt_tensor_download_async(const qt_tensor* t, double* host);
+
+/* ---- linear algebra (proj/src/linalg.cpp:40-64) --------------------------- */
+/* qr_reduced: m (p x q) = Q (p x k) R (k x q), k = min(p,q), R_ii real >= 0 */
+qt_status qt_qr_reduced(qt_ctx* ctx, const qt_tensor* m, qt_tensor** q_out, qt_tensor** r_out);
+/* lq_reduced: m (p x q) = L (p x k) Q (k x q), L_ii real >= 0 */
+qt_status qt_lq_reduced(qt_ctx* ctx, const qt_tensor* m, qt_tensor** l_out, qt_tensor** q_out);
+
+/* Batched complex GEMM on raw device pointers (interleaved complex128):
+ * C[b] = alpha * op(A[b]) op(B[b]) + beta * C[b], op: 0 = N, 1 = conjugate
+ * transpose.  Strides/leading dimensions in complex elements.  This is the
+ * contraction kernel behind contract() (proj/src/tensor.cpp:172-233). */
+qt_status qt_zgemm(qt_ctx* ctx, int op_a, int op_b, int64_t m, int64_t n, int64_t k, int batch,
+                   const void* a, int64_t lda, int64_t stride_a, const void* b, int64_t ldb, int64_t stride_b,
+                   void* c, int64_t ldc, int64_t stride_c, double alpha, double beta);
+
+/* ---- two-site updates (proj/include/qrtebd/gates.hpp:84-92) --------------- */
+/* apply_gate_qr     gates.cpp:343-386
+ * apply_gate_qr_cbe gates.cpp:388-450
+ * Outputs: b_m (d, chi_l, chi~), xi (chi~ x chi~), b_n (d, chi~, chi_r) and,
+ * for QR only, left_iso (d, chi_l, chi~) (pass NULL to skip it). */
+qt_status qt_apply_gate(qt_ctx* ctx, qt_scheme scheme, const qt_tensor* xi, const qt_tensor* b_m,
+                        const qt_tensor* b_n, const qt_tensor* u, const qt_policy* policy, qt_tensor** b_m_out,
+                        qt_tensor** xi_out, qt_tensor** b_n_out, qt_tensor** left_iso_out, qt_report* report);
+qt_status qt_apply_gate_qr(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m, const qt_tensor* b_n,
+                           const qt_tensor* u, const qt_policy* policy, qt_tensor** b_m_out, qt_tensor** xi_out,
+                           qt_tensor** b_n_out, qt_tensor** left_iso_out, qt_report* report);
+qt_status qt_apply_gate_qr_cbe(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m, const qt_tensor* b_n,
+                               const qt_tensor* u, const qt_policy* policy, qt_tensor** b_m_out,
+                               qt_tensor** xi_out, qt_tensor** b_n_out, qt_report* report);
+
+/* truncation_error_explicit, gates.cpp:464-485: ||theta - A (C B)||^2/||theta||^2 */
+qt_status qt_truncation_error_explicit(qt_ctx* ctx, const qt_tensor* theta, const qt_tensor* left,
+                                       const qt_tensor* center, const qt_tensor* right, double* out);
+
+/* ---- uniform TEBD step (gates.cpp:513-540) -------------------------------- */
+/* State of a UniformMPS (mps.hpp:18-26): sites[m] (d, chi, chi), bonds[m]
+ * (chi x chi).  layers[l] has parity parity[l] (0 even, 1 odd) and gate
+ * gates[l].  New handles are written to sites_out / bonds_out (the inputs
+ * are untouched); reports receives one entry per update (capacity
+ * *n_reports on entry, count on exit). */
+qt_status qt_tebd_step_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* const* sites, qt_tensor* const* bonds,
+                               uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates, qt_scheme scheme,
+                               const qt_policy* policy, qt_tensor** sites_out, qt_tensor** bonds_out,
+                               qt_bond_report* reports, uint64_t* n_reports);
+
+/* ---- observables (proj/src/mps.cpp) --------------------------------------- */
+/* expectation_local(UniformMPS), mps.cpp:168-186: <op> on a site given the
+ * bond matrix to its left and the site tensor; out = (re, im). */
+qt_status qt_expectation_local(qt_ctx* ctx, const qt_tensor* xi_left, const qt_tensor* b, const qt_tensor* op,
+                               double* out2);
+/* schmidt_values, mps.cpp:198-201: singular values of the bond matrix,
+ * descending; out has capacity *n on entry, count on exit. */
+qt_status qt_schmidt_values(qt_ctx* ctx, const qt_tensor* xi, double* out, uint64_t* n);
+/* right_defect, mps.cpp:34-36: || sum_i B^i B^i^H - 1 ||_max */
+qt_status qt_right_defect(qt_ctx* ctx, const qt_tensor* b, double* out);
+/* Bond energy <theta0|h|theta0>/<theta0|theta0>, theta0 = Xi B^m B^n
+ * (an extension, not in the reference). */
+qt_status qt_bond_energy(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m, const qt_tensor* b_n,
+                         const qt_tensor* h_bond, double* out);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+/* measured FP64 peak of this device in TFLOP/s: kind 0 = DMMA, 1 = DFMA */
+qt_status qt_fp64_peak(qt_ctx* ctx, int kind, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QRTEBD_C_H */

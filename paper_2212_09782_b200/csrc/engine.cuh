@@ -1,0 +1,94 @@
+// Device-resident engine state: stream, grow-only scratch arena, device
+// scalars and the host-visible pinned mirror used for reports.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "zgemm.cuh"
+
+namespace qt {
+
+enum Slot : int {
+  S_PHI = 0,
+  S_PHIEV,
+  S_THETA,
+  S_Y0,
+  S_X,
+  S_QM,
+  S_RM,
+  S_YH,
+  S_QP,
+  S_RP,
+  S_W,
+  S_QR_V,
+  S_QR_T,
+  S_QR_W,
+  S_QR_W2,
+  S_QR_PART,
+  S_GEMM_PART,
+  S_TILE_SUMS,
+  S_NORM_PART,
+  S_GRAM,
+  S_EIG_V,
+  S_EIG_W,
+  S_MISC,
+  S_MISC2,
+  S_COUNT
+};
+
+// device scalar indices (doubles)
+enum Scal : int {
+  SC_THETA2 = 0,  // ||theta||^2
+  SC_L2,          // ||L||^2 (or ||kept||^2 for CBE)
+  SC_RESID,       // explicit residual ||theta - approx||^2
+  SC_TMP0,
+  SC_TMP1,
+  SC_TMP2,
+  SC_TMP3,
+  SC_COUNT = 64
+};
+
+struct Engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::vector<void*> slot_ptr = std::vector<void*>(S_COUNT, nullptr);
+  std::vector<size_t> slot_bytes = std::vector<size_t>(S_COUNT, 0);
+  double* dscal = nullptr;   // device scalars
+  double* hscal = nullptr;   // pinned host mirror
+  unsigned* barrier = nullptr;  // grid-barrier words (count, generation)
+  int num_sms = kNumSMs;
+
+  void init(int dev, cudaStream_t st);
+  void destroy();
+  // grow-only scratch; contents are not preserved across growth
+  void* raw(int slot, size_t bytes);
+  double2* cbuf(int slot, size_t elems) { return static_cast<double2*>(raw(slot, elems * sizeof(double2))); }
+  double* dbuf(int slot, size_t elems) { return static_cast<double*>(raw(slot, elems * sizeof(double))); }
+  GemmScratch gemm_scratch();
+};
+
+// ---- kernels shared by the modules (aux.cu) -------------------------------
+// out = scale * [conj](permute(in)); rank <= 4, perm[k] = input axis of output axis k
+void permute(Engine& e, const double2* in, int rank, const long long* shape, const int* perm, bool conj,
+             double2* out, double scale = 1.0, const double* dscale = nullptr);
+// out[0] = sum |x|^2 over a (rows x cols, ld) matrix, deterministic
+void norm2(Engine& e, const double2* x, long long rows, long long cols, long long ld, double* out);
+// dst = src over rows x cols blocks with leading dimensions
+void copy2d(Engine& e, const double2* src, long long lds, double2* dst, long long ldd, long long rows,
+            long long cols);
+void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld);
+void check_finite(Engine& e, const double2* x, long long n, int* dflag);
+
+// ---- Householder QR (householder.cu) ----------------------------------------
+// Blocked Householder QR of the m x n row-major matrix a (ld lda), factored
+// in place (a is destroyed).  Writes the explicit thin Q (m x k, ld ldq) and
+// R (k x n, ld ldr), k = min(m, n), gauge-fixed so that diag(R) is real and
+// non-negative (proj/src/linalg.cpp:25-51).
+void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, double2* q, long long ldq,
+                double2* r, long long ldr);
+
+}  // namespace qt

@@ -1,0 +1,351 @@
+// Two-site QR-TEBD update on the device.
+//
+// Data flow of apply_gate_qr (proj/src/gates.cpp:343-386), all complex128 in
+// HBM, no host round trip inside the update:
+//
+//   phi(b,i,j,d)   = sum_g Bm[i,b,g] Bn[j,g,d]     DMMA GEMM, batched over j,
+//                                                   store permuted (gates.cpp:145-165)
+//   phiev(b,.,.,d) = U . phi(b,.,.,d)               DMMA GEMM, batched over b
+//                                                   (gates.cpp:168-171; the
+//                                                   transpose(2,0,1,3) is never
+//                                                   materialized)
+//   theta          = Xi . phiev                     DMMA GEMM  (gates.cpp:175-180)
+//   X = theta Y0^H ; QR ; Y^H = theta^H Q ; QR      DMMA GEMMs + K3 (gates.cpp:293-308)
+//   Xi~ = L/|L|, B~n = Q_n -> (d,eta,chi_r), B~m = phiev Q_n^H (permuted store),
+//   left_iso = Q_m -> (d,chi_l,eta), eps = ||theta - Q_m L Q_n||^2/||theta||^2
+#include <cmath>
+#include <cstring>
+
+#include "gate.cuh"
+
+namespace qt {
+
+unsigned long long expanded_dim(const qt_policy& p, unsigned long long chi, unsigned long long d) {
+  const auto rel = static_cast<unsigned long long>(std::ceil(p.delta_chi_rel * static_cast<double>(chi)));
+  const unsigned long long delta = std::max<unsigned long long>(p.delta_chi_abs, rel);
+  unsigned long long eta = std::min(d * chi, chi + delta);
+  if (p.chi_max_expansion != 0) eta = std::min<unsigned long long>(eta, p.chi_max_expansion);
+  return eta;
+}
+
+long long qr_eta(const qt_policy& p, const Dims& D) {
+  long long eta = static_cast<long long>(
+      std::min<unsigned long long>(expanded_dim(p, D.chi_n, D.d), p.chi_max));
+  return std::min({eta, D.rows(), D.cols()});
+}
+
+long long cbe_eta(const qt_policy& p, const Dims& D) {
+  const unsigned long long eta0 = expanded_dim(p, D.chi_n, D.d);
+  if (eta0 > static_cast<unsigned long long>(D.d * D.chi_n)) throw Error(Err::input, "bond expansion beyond d*chi");
+  return std::min({static_cast<long long>(eta0), D.rows(), D.cols()});
+}
+
+namespace {
+
+// dscal[out] = (den > 0) ? 1/den : 0 with den = sqrt(dscal[skip ? a : b])
+__global__ void inv_norm_kernel(double* dscal, int a, int b, int skip, int out) {
+  const double den = sqrt(dscal[skip ? a : b]);
+  dscal[out] = den > 0.0 ? 1.0 / den : 0.0;
+}
+
+__global__ void zero_flag_kernel(int* f) { *f = 0; }
+
+__global__ void trace_op_kernel(const double2* __restrict__ op, const double2* __restrict__ t2, int d,
+                                double* out2) {
+  // <O> = sum_{x,y} op[x,y] t2[y,x]   (proj/src/mps.cpp:173)
+  if (threadIdx.x == 0) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int x = 0; x < d; ++x)
+      for (int y = 0; y < d; ++y) s = cadd(s, cmul(op[x * d + y], t2[y * d + x]));
+    out2[0] = s.x;
+    out2[1] = s.y;
+  }
+}
+
+__global__ void defect_partial_kernel(const double2* __restrict__ g, long long n, double* part) {
+  __shared__ double sh[256];
+  double m = 0.0;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n * n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = e / n, c = e % n;
+    double2 v = g[e];
+    if (r == c) v.x -= 1.0;
+    m = fmax(m, hypot(v.x, v.y));
+  }
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void max_final_kernel(const double* __restrict__ part, int n, double* out) {
+  double m = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) m = fmax(m, part[i]);
+    *out = m;
+  }
+}
+
+// sum conj(a) b over n elements, two-pass deterministic
+__global__ void dot_partial_kernel(const double2* __restrict__ a, const double2* __restrict__ b, long long n,
+                                   double2* part) {
+  __shared__ double2 sh[256];
+  double2 s = make_double2(0.0, 0.0);
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    s = cadd(s, cmul(cconj(a[e]), b[e]));
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = cadd(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void dot_final_kernel(const double2* __restrict__ part, int n, double* out2) {
+  if (threadIdx.x == 0) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = 0; i < n; ++i) s = cadd(s, part[i]);
+    out2[0] = s.x;
+    out2[1] = s.y;
+  }
+}
+
+void gemm(Engine& e, Op oa, Op ob, long long M, long long N, long long K, const double2* A, long long lda,
+          const double2* B, long long ldb, double2* C, long long ldc, double alpha = 1.0, double beta = 0.0) {
+  GemmDesc g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.opA = oa;
+  g.opB = ob;
+  g.A = A;
+  g.lda = lda;
+  g.B = B;
+  g.ldb = ldb;
+  g.C = C;
+  g.ldc = ldc;
+  g.alpha = alpha;
+  g.beta = beta;
+  zgemm(g, e.gemm_scratch(), e.stream);
+}
+
+}  // namespace
+
+void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
+                 const double2* u, int out_scalar) {
+  const long long d = D.d, cl = D.chi_l, cm = D.chi_m, cn = D.chi_n, cr = D.chi_r;
+  const long long blk = cm * d * d * cr;
+  double2* phi = e.cbuf(S_PHI, blk);
+  double2* phiev = e.cbuf(S_PHIEV, blk);
+  double2* theta = e.cbuf(S_THETA, cl * d * d * cr);
+  const GemmScratch gs = e.gemm_scratch();
+  {
+    // phi(beta,i,j,delta): rows r = i*cm + beta of Bm viewed as (d*cm) x cn,
+    // batch j over Bn[j]; row r lands at beta*(d*d*cr) + i*(d*cr), batch at j*cr
+    GemmDesc g;
+    g.M = d * cm; g.N = cr; g.K = cn; g.batch = static_cast<int>(d);
+    g.A = bm; g.lda = cn; g.strideA = 0;
+    g.B = bn; g.ldb = cr; g.strideB = cn * cr;
+    g.C = phi; g.ldc = d * d * cr; g.rsplit = cm; g.ldc_hi = d * cr; g.strideC = cr;
+    zgemm(g, gs, e.stream);
+  }
+  {
+    // phiev[beta] (d^2 x cr) = U (d^2 x d^2) . phi[beta] (d^2 x cr)
+    GemmDesc g;
+    g.M = d * d; g.N = cr; g.K = d * d; g.batch = static_cast<int>(cm);
+    g.A = u; g.lda = d * d; g.strideA = 0;
+    g.B = phi; g.ldb = cr; g.strideB = d * d * cr;
+    g.C = phiev; g.ldc = cr; g.strideC = d * d * cr;
+    zgemm(g, gs, e.stream);
+  }
+  // theta = Xi (cl x cm) . phiev (cm x d*d*cr)
+  gemm(e, Op::N, Op::N, cl, d * d * cr, cm, xi, cm, phiev, d * d * cr, theta, d * d * cr);
+  norm2(e, theta, cl, d * d * cr, d * d * cr, e.dscal + out_scalar);
+}
+
+void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
+                   const double2* u, const qt_policy& pol, long long eta, const GateBuffers& out) {
+  const long long d = D.d, cl = D.chi_l, cm = D.chi_m, cn = D.chi_n, cr = D.chi_r;
+  const long long rows = D.rows(), cols = D.cols();
+  int* flag = reinterpret_cast<int*>(e.dscal + SC_TMP3);
+  zero_flag_kernel<<<1, 1, 0, e.stream>>>(flag);
+  build_theta(e, D, xi, bm, bn, u, SC_THETA2);
+  double2* phiev = e.cbuf(S_PHIEV, cm * d * d * cr);
+  double2* theta = e.cbuf(S_THETA, cl * d * d * cr);
+
+  double2* X = e.cbuf(S_X, rows * eta);
+  double2* Qm = e.cbuf(S_QM, rows * eta);
+  double2* Rm = e.cbuf(S_RM, eta * eta);
+  double2* YH = e.cbuf(S_YH, cols * eta);
+  double2* Qp = e.cbuf(S_QP, cols * eta);
+  double2* Rp = e.cbuf(S_RP, eta * eta);
+
+  // initial guess, gates.cpp:357-361
+  const bool y0_is_bn = (eta == cn);
+  const double2* y0 = theta;  // first eta rows of the grouped theta
+  if (y0_is_bn) {
+    double2* y = e.cbuf(S_Y0, cn * cols);
+    const long long shp[3] = {d, cn, cr};
+    const int perm[3] = {1, 0, 2};
+    permute(e, bn, 3, shp, perm, false, y);
+    y0 = y;
+  }
+  const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
+  for (int it = 0; it < sweeps; ++it) {
+    if (it == 0)
+      gemm(e, Op::N, Op::H, rows, eta, cols, theta, cols, y0, cols, X, eta);  // X = theta Y0^H
+    else
+      gemm(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);   // Y0 = Q_n = Qp^H
+    check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
+    qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta);
+    gemm(e, Op::H, Op::N, cols, eta, rows, theta, cols, Qm, eta, YH, eta);  // Y^H = theta^H Q_m
+    check_finite(e, YH, cols * eta, flag);
+    qr_inplace(e, YH, cols, eta, eta, Qp, eta, Rp, eta);  // Y^H = Qp Rp -> L = Rp^H, Q_n = Qp^H
+  }
+  norm2(e, Rp, eta, eta, eta, e.dscal + SC_L2);
+  inv_norm_kernel<<<1, 1, 0, e.stream>>>(e.dscal, SC_THETA2, SC_L2, pol.skip_renormalize ? 1 : 0, SC_TMP0);
+  QT_CUDA(cudaGetLastError());
+  {
+    // Xi~ = L / den = Rp^H / den   (gates.cpp:365-370)
+    const long long shp[2] = {eta, eta};
+    const int perm[2] = {1, 0};
+    permute(e, Rp, 2, shp, perm, true, out.xi, 1.0, e.dscal + SC_TMP0);
+  }
+  {
+    // B~n[j,k,delta] = Q_n[k,(j delta)] = conj(Qp[(j delta),k])   (gates.cpp:193-196)
+    const long long shp[3] = {d, cr, eta};
+    const int perm[3] = {0, 2, 1};
+    permute(e, Qp, 3, shp, perm, true, out.b_n);
+  }
+  {
+    // B~m[i,beta,k] = sum_{j,delta} phiev[beta,i,j,delta] conj(B~n[j,k,delta])
+    //             = (phiev (cm*d x d*cr) . Qp)[(beta i), k]   (gates.cpp:186-190)
+    GemmDesc g;
+    g.M = cm * d; g.N = eta; g.K = cols;
+    g.A = phiev; g.lda = cols;
+    g.B = Qp; g.ldb = eta;
+    g.C = out.b_m; g.ldc = cm * eta; g.rsplit = d; g.ldc_hi = eta;
+    zgemm(g, e.gemm_scratch(), e.stream);
+  }
+  if (out.left_iso) {
+    // left_iso = Q_m (cl, d, eta) -> (d, cl, eta)   (gates.cpp:198-201)
+    const long long shp[3] = {cl, d, eta};
+    const int perm[3] = {1, 0, 2};
+    permute(e, Qm, 3, shp, perm, false, out.left_iso);
+  }
+  if (pol.compute_explicit_error) {
+    // W = L Q_n = Rp^H Qp^H (eta x cols), then sum |theta - Q_m W|^2 (gates.cpp:464-485)
+    double2* W = e.cbuf(S_W, eta * cols);
+    gemm(e, Op::H, Op::H, eta, cols, eta, Rp, eta, Qp, eta, W, cols);
+    GemmDesc g;
+    g.M = rows; g.N = cols; g.K = eta;
+    g.A = Qm; g.lda = eta;
+    g.B = W; g.ldb = cols;
+    g.C = theta; g.ldc = cols;
+    g.mode = GemmMode::resid;
+    zgemm(g, e.gemm_scratch(), e.stream, e.dscal + SC_RESID);
+  }
+}
+
+HostReport read_report(Engine& e) {
+  QT_CUDA(cudaMemcpyAsync(e.hscal, e.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  HostReport r;
+  r.theta2 = e.hscal[SC_THETA2];
+  r.kept2 = e.hscal[SC_L2];
+  r.resid = e.hscal[SC_RESID];
+  int flag = 0;
+  std::memcpy(&flag, &e.hscal[SC_TMP3], sizeof(int));
+  r.finite = flag == 0;
+  return r;
+}
+
+// ------------------------------------------------------------ observables
+void expectation_local(Engine& e, const double2* xi, long long chi_l, const double2* b, long long d,
+                       long long chi_r, const double2* op, double* out2_host) {
+  // M = Xi^H Xi ; lambda = conj(M) (mps.cpp:44-46)
+  // t1[i] = M^H . B[i]  (= sum_a lambda[a,a'] B[i,a,b], mps.cpp:171)
+  // t2 = t1 (d x chi_l*chi_r) . B^H  (mps.cpp:172) ; <O> = tr(op t2^T)
+  double2* M = e.cbuf(S_MISC, chi_l * chi_l + d * d + 8);
+  double2* t2 = M + chi_l * chi_l;
+  double2* t1 = e.cbuf(S_MISC2, d * chi_l * chi_r);
+  gemm(e, Op::H, Op::N, chi_l, chi_l, chi_l, xi, chi_l, xi, chi_l, M, chi_l);
+  {
+    GemmDesc g;
+    g.M = chi_l; g.N = chi_r; g.K = chi_l; g.batch = static_cast<int>(d);
+    g.opA = Op::H; g.A = M; g.lda = chi_l; g.strideA = 0;
+    g.B = b; g.ldb = chi_r; g.strideB = chi_l * chi_r;
+    g.C = t1; g.ldc = chi_r; g.strideC = chi_l * chi_r;
+    zgemm(g, e.gemm_scratch(), e.stream);
+  }
+  gemm(e, Op::N, Op::H, d, d, chi_l * chi_r, t1, chi_l * chi_r, b, chi_l * chi_r, t2, d);
+  trace_op_kernel<<<1, 32, 0, e.stream>>>(op, t2, static_cast<int>(d), e.dscal + SC_TMP1);
+  QT_CUDA(cudaGetLastError());
+  QT_CUDA(cudaMemcpyAsync(out2_host, e.dscal + SC_TMP1, 2 * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+}
+
+double right_defect(Engine& e, const double2* b, long long d, long long chi_l, long long chi_r) {
+  // sum_i B^i B^i^H - 1 (mps.cpp:34-36): permute to (chi_l, d, chi_r), Gram
+  double2* bp = e.cbuf(S_MISC2, d * chi_l * chi_r);
+  double2* g = e.cbuf(S_MISC, chi_l * chi_l);
+  const long long shp[3] = {d, chi_l, chi_r};
+  const int perm[3] = {1, 0, 2};
+  permute(e, b, 3, shp, perm, false, bp);
+  gemm(e, Op::N, Op::H, chi_l, chi_l, d * chi_r, bp, d * chi_r, bp, d * chi_r, g, chi_l);
+  double* part = e.dbuf(S_NORM_PART, 296);
+  defect_partial_kernel<<<148, 256, 0, e.stream>>>(g, chi_l, part);
+  max_final_kernel<<<1, 32, 0, e.stream>>>(part, 148, e.dscal + SC_TMP1);
+  double out = 0;
+  QT_CUDA(cudaMemcpyAsync(&out, e.dscal + SC_TMP1, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  return out;
+}
+
+double bond_energy(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
+                   const double2* h) {
+  // E = <theta0|h theta0>/<theta0|theta0>, theta0 = Xi Bm Bn
+  const long long d = D.d;
+  const long long n = D.chi_l * d * d * D.chi_r;
+  double2* ident = e.cbuf(S_EIG_V, d * d * d * d + n);
+  double2* theta_h = ident + d * d * d * d;
+  set_identity(e, ident, d * d, d * d, d * d);
+  build_theta(e, D, xi, bm, bn, h, SC_TMP1);
+  copy2d(e, e.cbuf(S_THETA, n), n, theta_h, n, 1, n);
+  build_theta(e, D, xi, bm, bn, ident, SC_TMP2);
+  const double2* theta0 = e.cbuf(S_THETA, n);
+  double2* part = e.cbuf(S_NORM_PART, 296);
+  dot_partial_kernel<<<148, 256, 0, e.stream>>>(theta0, theta_h, n, part);
+  dot_final_kernel<<<1, 32, 0, e.stream>>>(part, 148, e.dscal + SC_TMP0);
+  double hv[4] = {0, 0, 0, 0};
+  QT_CUDA(cudaMemcpyAsync(hv, e.dscal + SC_TMP0, 3 * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  // hv[0] = Re<theta0|h theta0>, hv[2] = ||theta0||^2 (SC_TMP2)
+  return hv[2] > 0 ? hv[0] / hv[2] : 0.0;
+}
+
+double explicit_error(Engine& e, const double2* theta, long long rows, long long cols, const double2* left,
+                      long long kdim, const double2* center, long long kdim2, const double2* right) {
+  double2* W = e.cbuf(S_W, kdim * cols);
+  gemm(e, Op::N, Op::N, kdim, cols, kdim2, center, kdim2, right, cols, W, cols);
+  norm2(e, theta, rows, cols, cols, e.dscal + SC_TMP1);
+  GemmDesc g;
+  g.M = rows; g.N = cols; g.K = kdim;
+  g.A = left; g.lda = kdim;
+  g.B = W; g.ldb = cols;
+  g.C = const_cast<double2*>(theta); g.ldc = cols;
+  g.mode = GemmMode::resid;
+  zgemm(g, e.gemm_scratch(), e.stream, e.dscal + SC_TMP2);
+  double hv[2];
+  QT_CUDA(cudaMemcpyAsync(hv, e.dscal + SC_TMP1, 2 * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  if (hv[0] == 0.0) return 0.0;
+  return hv[1] / hv[0];
+}
+
+}  // namespace qt

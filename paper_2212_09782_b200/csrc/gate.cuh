@@ -1,0 +1,77 @@
+// Two-site update engine (apply_gate_qr / apply_gate_qr_cbe) and the
+// observable contractions, device-resident.
+#pragma once
+
+#include <functional>
+
+#include "engine.cuh"
+#include "../../include/qrtebd_c.h"
+
+namespace qt {
+
+struct Dims {
+  long long d = 0, chi_l = 0, chi_m = 0, chi_n = 0, chi_r = 0;
+  long long rows() const { return chi_l * d; }
+  long long cols() const { return d * chi_r; }
+};
+
+// TruncationPolicy::expanded_dim, proj/src/gates.cpp:94-101
+unsigned long long expanded_dim(const qt_policy& p, unsigned long long chi, unsigned long long d);
+
+// working width of apply_gate_qr, proj/src/gates.cpp:354-355
+long long qr_eta(const qt_policy& p, const Dims& D);
+// working width of apply_gate_qr_cbe, proj/src/gates.cpp:398-401 (throws InputError past d*chi)
+long long cbe_eta(const qt_policy& p, const Dims& D);
+
+struct GateBuffers {
+  double2* b_m = nullptr;       // (d, chi_m, chi~)
+  double2* xi = nullptr;        // chi~ x chi~
+  double2* b_n = nullptr;       // (d, chi~, chi_r)
+  double2* left_iso = nullptr;  // (d, chi_l, chi~) or nullptr
+};
+
+struct HostReport {
+  double theta2 = 0, kept2 = 0, resid = 0;
+  bool finite = true;
+};
+
+// theta build (K1a/K1b/K1c, proj/src/gates.cpp:123-182): fills the engine
+// slots S_PHIEV (beta,i,j,delta) and S_THETA (alpha,i,j,delta); ||theta||^2 is
+// written to dscal[out_scalar].
+void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
+                 const double2* u, int out_scalar);
+
+// apply_gate_qr (proj/src/gates.cpp:343-386) with outputs written into
+// caller-allocated buffers sized for eta = qr_eta(policy, D).  Fully
+// asynchronous on e.stream; the report scalars stay in e.dscal.
+void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
+                   const double2* u, const qt_policy& pol, long long eta, const GateBuffers& out);
+
+// Collects the report of the last gate_qr_async / CBE update (synchronizes).
+HostReport read_report(Engine& e);
+
+// apply_gate_qr_cbe (proj/src/gates.cpp:388-450).  Data-dependent kept
+// width: allocates outputs through `alloc` once kk is known (one host sync).
+struct CbeResult {
+  long long eta = 0, kk = 0;
+  HostReport rep;
+};
+CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
+                   const double2* u, const qt_policy& pol, const std::function<GateBuffers(long long)>& alloc);
+
+// eigh of a Hermitian n x n matrix on the device (proj/src/linalg.cpp:79-101):
+// eigenvalues descending into w (device), eigenvectors as columns of v (device, ld n)
+void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v);
+// singular values of an arbitrary p x q matrix, descending (device out, min(p,q))
+void singular_values_device(Engine& e, const double2* m, long long p, long long q, double* s);
+
+// observables (proj/src/mps.cpp)
+void expectation_local(Engine& e, const double2* xi, long long chi_l, const double2* b, long long d,
+                       long long chi_r, const double2* op, double* out2_host);
+double right_defect(Engine& e, const double2* b, long long d, long long chi_l, long long chi_r);
+double bond_energy(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
+                   const double2* h);
+double explicit_error(Engine& e, const double2* theta, long long rows, long long cols, const double2* left,
+                      long long kdim, const double2* center, long long kdim2, const double2* right);
+
+}  // namespace qt

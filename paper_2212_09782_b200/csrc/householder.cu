@@ -1,0 +1,352 @@
+// K3: blocked Householder QR with explicit thin Q and the reference gauge.
+//
+// Replaces qr_reduced / fix_qr_gauge (proj/src/linalg.cpp:25-51, Eigen
+// HouseholderQR + householderQ()*I).  LAPACK zgeqrf/zlarfg/zlarft/zungqr
+// conventions: H_c = I - tau_c v_c v_c^H with v_c[c] = 1, beta real,
+// tau = 0 for an exactly-zero column (rank-deficient blocks, e.g. product
+// states, proj/tests/test_gates.cc:354-367); Q = H_0 ... H_{k-1}.
+//
+// Panel (32 columns): one cooperative kernel.  The panel rows are spread
+// over up to 148 CTAs and kept in shared memory; each column needs ONE
+// grid-wide reduction, because the norm of the column tail, the projections
+// x^H a_k of the later columns and the T-factor products V^H v_c all come out
+// of the same pass (lane k of every warp owns panel column k).  Partial sums
+// are combined in a fixed order on every CTA, so the factorization is
+// bitwise deterministic.
+//
+// Trailing update and Q formation: the compact-WY block reflector
+// I - V T V^H applied with three DMMA GEMMs (V^H A, T^H W, A - V W2).
+#include <cooperative_groups.h>
+
+#include "engine.cuh"
+
+namespace qt {
+namespace {
+
+constexpr int NB = 32;
+constexpr int PANEL_THREADS = 256;
+constexpr int PANEL_WARPS = PANEL_THREADS / 32;
+
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct PanelArgs {
+  double2* A;  // panel top-left, row-major, ld lda
+  long long lda;
+  long long mp;  // panel rows
+  int nbp;       // panel columns (<= 32)
+  int rpc;       // rows per CTA
+  double2* V;    // V panel top-left, ld ldv (unit lower trapezoidal, written here)
+  long long ldv;
+  double2* T;      // 32 x 32 upper triangular T factor
+  double2* part;   // [2][grid][32] partial sums
+  double2* diag;   // [2][32] broadcast of the current diagonal row
+  unsigned* bar;   // grid barrier words
+};
+
+__global__ void __launch_bounds__(PANEL_THREADS, 1) panel_kernel(PanelArgs a) {
+  extern __shared__ double2 psm[];
+  double2* P = psm;                            // [rpc][32]
+  double2* red = P + size_t(a.rpc) * NB;       // [8][32]
+  double2* Ts = red + PANEL_WARPS * NB;        // [32][32]
+  double2* ssum = Ts + NB * NB;                // [32]
+  double2* zs = ssum + NB;                     // [32]
+
+  const int w = threadIdx.x >> 5, k = threadIdx.x & 31;
+  const unsigned G = gridDim.x;
+  const long long r0 = static_cast<long long>(blockIdx.x) * a.rpc;
+  const int nloc = static_cast<int>(max(0LL, min(static_cast<long long>(a.rpc), a.mp - r0)));
+  const int nbp = a.nbp;
+
+  for (int lr = w; lr < a.rpc; lr += PANEL_WARPS)
+    P[lr * NB + k] = (lr < nloc && k < nbp) ? a.A[(r0 + lr) * a.lda + k] : make_double2(0.0, 0.0);
+  for (int e = threadIdx.x; e < NB * NB; e += PANEL_THREADS) Ts[e] = make_double2(0.0, 0.0);
+  __syncthreads();
+
+  for (int c = 0; c < nbp; ++c) {
+    const int par = c & 1;
+    // ---- phase 1: one pass over the local rows below the diagonal
+    //   lane k >= c : g_k = sum conj(x_r) a_rk   (k == c gives ||x||^2)
+    //   lane k <  c : h_k = sum conj(v_rk) x_r   (T-factor products)
+    double2 acc = make_double2(0.0, 0.0);
+    for (int lr = w; lr < nloc; lr += PANEL_WARPS) {
+      if (r0 + lr <= c) continue;
+      const double2 x = P[lr * NB + c];
+      const double2 y = P[lr * NB + k];
+      const double2 u = (k >= c) ? x : y;
+      const double2 v = (k >= c) ? y : x;
+      acc.x = fma(u.x, v.x, fma(u.y, v.y, acc.x));
+      acc.y = fma(u.x, v.y, fma(-u.y, v.x, acc.y));
+    }
+    red[w * NB + k] = acc;
+    __syncthreads();
+    if (w == 0) {
+      double2 s = red[k];
+      for (int ww = 1; ww < PANEL_WARPS; ++ww) s = cadd(s, red[ww * NB + k]);
+      a.part[(size_t(par) * G + blockIdx.x) * NB + k] = s;
+    }
+    if (blockIdx.x == 0 && w == 1) a.diag[par * NB + k] = P[c * NB + k];
+    grid_sync(a.bar, G);
+
+    // ---- phase 2: combine partials (fixed order) and form the reflector
+    if (w == 0) {
+      double2 s = make_double2(0.0, 0.0);
+      for (unsigned b = 0; b < G; ++b) s = cadd(s, __ldcg(&a.part[(size_t(par) * G + b) * NB + k]));
+      ssum[k] = s;
+    }
+    __syncthreads();
+    const double2 alpha = __ldcg(&a.diag[par * NB + c]);
+    const double xnorm2 = ssum[c].x;
+    double2 tau, scale;
+    double beta;
+    if (xnorm2 == 0.0 && alpha.y == 0.0) {
+      tau = make_double2(0.0, 0.0);
+      beta = alpha.x;
+      scale = make_double2(0.0, 0.0);
+    } else {
+      const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2);
+      beta = alpha.x >= 0.0 ? -nrm : nrm;
+      tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+      // scale = 1 / (alpha - beta)
+      const double2 den = make_double2(alpha.x - beta, alpha.y);
+      const double dd = den.x * den.x + den.y * den.y;
+      scale = make_double2(den.x / dd, -den.y / dd);
+    }
+    const double2 ctau = cconj(tau);
+    // w_k = a_ck + conj(scale) g_k  for k > c
+    const double2 a_ck = __ldcg(&a.diag[par * NB + k]);
+    const double2 wk = cadd(a_ck, cmul(cconj(scale), ssum[k]));
+    const double2 ctw = cmul(ctau, wk);  // conj(tau) w_k
+
+    // T column c (zlarft, forward/columnwise): T[0:c,c] = T[0:c,0:c] z,
+    // z_i = -tau (conj(v_c,i) + scale h_i)
+    if (w == 0) {
+      double2 z = make_double2(0.0, 0.0);
+      if (k < c) z = cmul(make_double2(-tau.x, -tau.y), cadd(cconj(a_ck), cmul(scale, ssum[k])));
+      zs[k] = z;
+      __syncwarp();
+      if (k < c) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int l = k; l < c; ++l) t = cadd(t, cmul(Ts[k * NB + l], zs[l]));
+        Ts[k * NB + c] = t;
+      } else if (k == c) {
+        Ts[c * NB + c] = tau;
+      }
+    }
+
+    // ---- phase 3: apply H_c^H to the local rows, store v in column c
+    for (int lr = w; lr < nloc; lr += PANEL_WARPS) {
+      const long long gr = r0 + lr;
+      if (gr < c) continue;
+      if (gr == c) {
+        if (k > c && k < nbp) P[lr * NB + k] = csub(P[lr * NB + k], ctw);
+        __syncwarp();
+        if (k == c) P[lr * NB + c] = make_double2(beta, 0.0);
+      } else {
+        const double2 vr = cmul(scale, P[lr * NB + c]);
+        __syncwarp();
+        if (k > c && k < nbp) P[lr * NB + k] = csub(P[lr * NB + k], cmul(vr, ctw));
+        if (k == c) P[lr * NB + c] = vr;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- write back R/V to A, the dense unit-lower V panel, and T
+  for (int lr = w; lr < nloc; lr += PANEL_WARPS) {
+    const long long gr = r0 + lr;
+    if (k < nbp) {
+      const double2 v = P[lr * NB + k];
+      a.A[gr * a.lda + k] = v;
+      a.V[gr * a.ldv + k] =
+          gr > k ? v : (gr == k ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0));
+    }
+  }
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < NB * NB; e += PANEL_THREADS) a.T[e] = Ts[e];
+}
+
+// R_ii = |R_ii|, Q[:, i] *= ph_i, R[i, :] *= conj(ph_i), ph_i = R_ii/|R_ii|
+__global__ void gauge_q_kernel(const double2* __restrict__ a, long long lda, double2* q, long long ldq,
+                               long long m, long long k) {
+  const long long total = m * k;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = e / k, c = e % k;
+    const double2 d = a[c * lda + c];
+    const double ad = hypot(d.x, d.y);
+    if (ad == 0.0) continue;
+    const double2 ph = make_double2(d.x / ad, d.y / ad);
+    q[r * ldq + c] = cmul(q[r * ldq + c], ph);
+  }
+}
+
+__global__ void gauge_r_kernel(const double2* __restrict__ a, long long lda, double2* r, long long ldr,
+                               long long k, long long n) {
+  const long long total = k * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / n, c = e % n;
+    double2 v = make_double2(0.0, 0.0);
+    if (c >= i) {
+      const double2 d = a[i * lda + i];
+      const double ad = hypot(d.x, d.y);
+      if (c == i) {
+        v = make_double2(ad, 0.0);
+      } else {
+        v = a[i * lda + c];
+        if (ad != 0.0) v = cmul(v, make_double2(d.x / ad, -d.y / ad));
+      }
+    }
+    r[i * ldr + c] = v;
+  }
+}
+
+int grid_for(long long total) {
+  const long long b = ceil_div(total, 256);
+  return static_cast<int>(b < 16LL * kNumSMs ? (b > 0 ? b : 1) : 16LL * kNumSMs);
+}
+
+void launch_panel(Engine& e, const PanelArgs& base, long long mp) {
+  // ~128 rows per CTA, at most one CTA per SM (co-residency for the grid
+  // barrier), at least 32 rows so CTA 0 owns the whole diagonal block
+  long long G = std::min<long long>(e.num_sms, std::max<long long>(1, ceil_div(mp, 128)));
+  long long rpc = std::max<long long>(NB, ceil_div(mp, G));
+  rpc = ceil_div(rpc, 8) * 8;
+  G = ceil_div(mp, rpc);
+  if (rpc > 1024) throw Error(Err::capacity, "QR panel taller than 148 x 1024 rows");
+  PanelArgs a = base;
+  a.rpc = static_cast<int>(rpc);
+  const size_t smem = (size_t(rpc) * NB + PANEL_WARPS * NB + NB * NB + 2 * NB) * sizeof(double2);
+  static size_t attr = 0;
+  if (smem > attr) {
+    QT_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(G));
+  cfg.blockDim = dim3(PANEL_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = e.stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeCooperative;
+  attrs[0].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  QT_CUDA(cudaLaunchKernelEx(&cfg, panel_kernel, a));
+}
+
+}  // namespace
+
+void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, double2* q, long long ldq,
+                double2* r, long long ldr) {
+  const long long k = std::min(m, n);
+  if (k == 0) return;
+  const long long npan = ceil_div(k, NB);
+  const long long kp = npan * NB;
+  double2* V = e.cbuf(S_QR_V, static_cast<size_t>(m) * kp);
+  double2* T = e.cbuf(S_QR_T, static_cast<size_t>(npan) * NB * NB);
+  double2* W = e.cbuf(S_QR_W, static_cast<size_t>(NB) * n);
+  double2* W2 = e.cbuf(S_QR_W2, static_cast<size_t>(NB) * n);
+  double2* part = e.cbuf(S_QR_PART, static_cast<size_t>(2) * kNumSMs * NB + 2 * NB);
+  const GemmScratch gs = e.gemm_scratch();
+
+  PanelArgs base{};
+  base.lda = lda;
+  base.ldv = kp;
+  base.part = part;
+  base.diag = part + 2 * kNumSMs * NB;
+  base.bar = e.barrier;
+
+  for (long long p = 0; p < npan; ++p) {
+    const long long j = p * NB;
+    const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+    const long long mp = m - j;
+    PanelArgs pa = base;
+    pa.A = a + j * lda + j;
+    pa.mp = mp;
+    pa.nbp = nbp;
+    pa.V = V + j * kp + p * NB;
+    pa.T = T + p * NB * NB;
+    launch_panel(e, pa, mp);
+    const long long ntr = n - j - nbp;
+    if (ntr > 0) {
+      GemmDesc g;
+      // W = V^H A_trail
+      g.M = nbp; g.N = ntr; g.K = mp;
+      g.opA = Op::H; g.A = pa.V; g.lda = kp;
+      g.opB = Op::N; g.B = a + j * lda + j + nbp; g.ldb = lda;
+      g.C = W; g.ldc = ntr;
+      zgemm(g, gs, e.stream);
+      // W2 = T^H W
+      GemmDesc g2;
+      g2.M = nbp; g2.N = ntr; g2.K = nbp;
+      g2.opA = Op::H; g2.A = pa.T; g2.lda = NB;
+      g2.opB = Op::N; g2.B = W; g2.ldb = ntr;
+      g2.C = W2; g2.ldc = ntr;
+      zgemm(g2, gs, e.stream);
+      // A_trail -= V W2
+      GemmDesc g3;
+      g3.M = mp; g3.N = ntr; g3.K = nbp;
+      g3.opA = Op::N; g3.A = pa.V; g3.lda = kp;
+      g3.opB = Op::N; g3.B = W2; g3.ldb = ntr;
+      g3.C = a + j * lda + j + nbp; g3.ldc = lda;
+      g3.alpha = -1.0; g3.beta = 1.0;
+      zgemm(g3, gs, e.stream);
+    }
+  }
+
+  // explicit thin Q = H_0 ... H_{k-1} I[:, :k], block reflectors backward
+  set_identity(e, q, m, k, ldq);
+  for (long long p = npan - 1; p >= 0; --p) {
+    const long long j = p * NB;
+    const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+    const long long mp = m - j, nq = k - j;
+    const double2* Vp = V + j * kp + p * NB;
+    const double2* Tp = T + p * NB * NB;
+    double2* Qs = q + j * ldq + j;
+    GemmDesc g;
+    g.M = nbp; g.N = nq; g.K = mp;
+    g.opA = Op::H; g.A = Vp; g.lda = kp;
+    g.opB = Op::N; g.B = Qs; g.ldb = ldq;
+    g.C = W; g.ldc = nq;
+    zgemm(g, gs, e.stream);
+    GemmDesc g2;
+    g2.M = nbp; g2.N = nq; g2.K = nbp;
+    g2.opA = Op::N; g2.A = Tp; g2.lda = NB;
+    g2.opB = Op::N; g2.B = W; g2.ldb = nq;
+    g2.C = W2; g2.ldc = nq;
+    zgemm(g2, gs, e.stream);
+    GemmDesc g3;
+    g3.M = mp; g3.N = nq; g3.K = nbp;
+    g3.opA = Op::N; g3.A = Vp; g3.lda = kp;
+    g3.opB = Op::N; g3.B = W2; g3.ldb = nq;
+    g3.C = Qs; g3.ldc = ldq;
+    g3.alpha = -1.0; g3.beta = 1.0;
+    zgemm(g3, gs, e.stream);
+  }
+
+  gauge_q_kernel<<<grid_for(m * k), 256, 0, e.stream>>>(a, lda, q, ldq, m, k);
+  QT_CUDA(cudaGetLastError());
+  gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
+  QT_CUDA(cudaGetLastError());
+}
+
+}  // namespace qt
