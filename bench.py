@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 QR-TEBD bond update (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Workload (default, BASELINE.json configs[1] = SURVEY.md C2): global quench of
+the d=5 quantum clock model, uniform MPS with unit cell L=2, chi=256, QR
+truncation (chi_max = chi, so eta = chi), complex128, Trotter order 2
+(3 dependent two-site updates per step), g=2, dt=0.05, explicit truncation
+error on (the quench default, proj/include/qrtebd/gates.hpp:51).  Synthetic
+steady-state input at fixed chi: random right isometries and a Gaussian bond
+matrix (the bench_cell recipe, proj/src/run.cpp:345-381).
+
+A "step" is one tebd_step (proj/src/gates.cpp:513-540) through the C-ABI
+qt_tebd_step_uniform with the state resident in HBM.  `value` = Trotter
+steps/s; `e2e` = the same metric with the state copied host->device from
+pinned memory before and device->host after every step.  The uniform cell
+does not shard (3 strictly dependent updates): N GPUs run N replicas
+("replicas only"), value = N x per-replica rate from the max time
+over ranks.
+
+--impl reference times the reference algorithm on the host CPU (the NumPy/LAPACK
+oracle port, oracle/qrtebd_oracle.py; the C++/Eigen reference cannot be built
+here) on the same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Trotter steps/sec (2-site QR updates/sec) vs chi,d; FP64 tensor-pipe % of peak"
+
+CONFIGS = {
+    # name: (description, d, chi, scheme, explicit, L)
+    "c1": ("C1 iTEBD transverse-field Ising (clock d=2), L=2, chi=64, qr", 2, 64, "qr", True),
+    "c2": ("C2 clock-model quench d=5, chi=256, uniform L=2, qr (eta=chi), explicit error on", 5, 256, "qr", True),
+    "north": ("north-star clock quench d=5, chi=1024, uniform L=2, qr (eta=chi), explicit error on", 5, 1024, "qr",
+              True),
+    "c3": ("C3 clock d=10, chi=1024, uniform L=2, qr (eta=chi), explicit error on", 10, 1024, "qr", True),
+}
+
+
+def flops_per_update(d, chi, eta, kk, explicit):
+    """8 flops per complex MAC."""
+    f = 8.0 * (2 * d * d * chi ** 3 + d ** 4 * chi ** 2 + 2 * d * d * chi * chi * eta + d * d * chi * chi * kk)
+    f += 2.0 * (16.0 * (d * chi) * eta * eta - 16.0 / 3.0 * eta ** 3)
+    if explicit:
+        f += 8.0 * (eta * eta * d * chi + d * d * chi * chi * eta)
+    return f
+
+
+def synthetic_state(d, chi, seed=0x51AB):
+    """Random right-canonical L=2 state at fixed chi (bench_cell recipe)."""
+    rng = np.random.default_rng([seed, d, chi])
+
+    def right_iso():
+        g = rng.standard_normal((d * chi, chi)) + 1j * rng.standard_normal((d * chi, chi))
+        q, r = np.linalg.qr(g)  # columns orthonormal -> rows of q^H orthonormal
+        q = q * (np.diag(r) / np.abs(np.diag(r)))
+        qh = q.conj().T  # (chi, d*chi) with orthonormal rows
+        return np.ascontiguousarray(qh.reshape(chi, d, chi).transpose(1, 0, 2))
+
+    def bond():
+        x = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+        return x / np.linalg.norm(x)
+
+    return [right_iso(), right_iso()], [bond(), bond()]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        reasons = set()
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if len(s) > 2 + k and s[2 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_rate(d, chi, scheme, explicit, budget_s, min_steps=1, warmup=0, seed=0x51AB):
+    """Reference algorithm on the host cores: the oracle port (test infra)."""
+    from oracle import qrtebd_oracle as ref
+    from paper_2212_09782_b200 import model
+    sites, bonds = synthetic_state(d, chi, seed)
+    st = ref.UniformMPS(d, [s.copy() for s in sites], [b.copy() for b in bonds])
+    sched = [(p, model.make_gate(model.bond_hamiltonian(d, 2.0), dte)) for p, dte in model.layer_structure(0.05, 2)]
+    pol = ref.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=explicit)
+    for _ in range(warmup):
+        st, _ = ref.tebd_step_uniform(st, sched, scheme, pol)
+    n, t0 = 0, time.perf_counter()
+    while n < min_steps or (time.perf_counter() - t0) < budget_s:
+        st, _ = ref.tebd_step_uniform(st, sched, scheme, pol)
+        n += 1
+        if time.perf_counter() - t0 > budget_s and n >= min_steps:
+            break
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if rank != 0:
+        return 0
+    desc, d, chi, scheme, explicit = cfg
+    # each "step" is a bounded sample: one full Trotter step of the oracle
+    rate, n, dt = cpu_reference_rate(d, chi, scheme, explicit, budget_s=0.0, min_steps=max(1, args.steps),
+                                     warmup=min(args.warmup, 1))
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
+        "steps": n, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 / rate, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+        "config": {"workload": desc, "d": d, "chi": chi, "scheme": scheme, "cell_length": 2,
+                   "explicit_error": explicit, "parallelism": "replicas"},
+        "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} full Trotter steps of the NumPy/LAPACK oracle (OpenBLAS, {cores} threads)"},
+        "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    from paper_2212_09782_b200 import _capi, model
+    from paper_2212_09782_b200 import qrtebd as q
+
+    ws, rank, local = dist_setup()
+    desc, d, chi, scheme, explicit = cfg
+    warmup = max(3, args.warmup)
+    ctx = _capi.Context(local)
+    lib = ctx.lib
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    dmma_peak = ctx.fp64_peak(0)
+
+    sites_h, bonds_h = synthetic_state(d, chi)
+    state0 = q.UniformMPS.from_numpy(ctx, d, sites_h, bonds_h)
+    sched_h = [(p, model.make_gate(model.bond_hamiltonian(d, 2.0), dte)) for p, dte in model.layer_structure(0.05, 2)]
+    sched = [(p, ctx.tensor(u)) for p, u in sched_h]
+    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=explicit)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > 126 MB L2
+
+    state = state0
+    for _ in range(warmup):
+        state, reps = q.tebd_step(state, sched, scheme, pol, ctx)
+    assert all(r.report.chi_after == chi for r in reps)
+
+    # ---------------- timed region: device-resident state
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(ws)
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    launches0 = lib.qt_kernel_launches()
+    _capi.check(lib.qt_profile_begin(ctx.h))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between timed steps, outside the event pair
+        evs[k][0].record(stream)
+        state, reps = q.tebd_step(state, sched, scheme, pol, ctx)
+        evs[k][1].record(stream)
+    ctx.synchronize()
+    gf, gms, gl = (np.zeros(1), np.zeros(1), np.zeros(1, dtype=np.uint64))
+    gfl, gmsl, gll = _capi.C.c_double(), _capi.C.c_double(), _capi.C.c_uint64()
+    _capi.check(lib.qt_profile_end(ctx.h, _capi.C.byref(gfl), _capi.C.byref(gmsl), _capi.C.byref(gll)))
+    launches = lib.qt_kernel_launches() - launches0
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = max_over_ranks(sum(step_ms), ws)
+    ms_per_step = tot_ms / args.steps
+    value = ws * 1e3 / ms_per_step
+
+    # ---------------- e2e: host (pinned) state in, host state out every step
+    flat_in = [torch.from_numpy(np.ascontiguousarray(a).view(np.float64)).pin_memory() for a in sites_h + bonds_h]
+    h2d = sum(t.numel() * 8 for t in flat_in)
+    outs_pinned = [torch.empty_like(t).pin_memory() for t in flat_in]
+    dev_in = [ctx.empty(a.shape) for a in sites_h + bonds_h]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(ws)
+    ctx.synchronize()
+    e0.record(stream)
+    for k in range(args.steps):
+        for t, hbuf in zip(dev_in, flat_in):
+            _capi.check(lib.qt_tensor_upload_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
+        st_in = q.UniformMPS(d, dev_in[:2], dev_in[2:])
+        st_out, _ = q.tebd_step(st_in, sched, scheme, pol, ctx)
+        for t, hbuf in zip(st_out.site_tensors + st_out.bond_matrices, outs_pinned):
+            _capi.check(lib.qt_tensor_download_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
+    e1.record(stream)
+    ctx.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws) / args.steps
+    d2h = sum(t.numel() * 8 for t in outs_pinned)
+
+    # ---------------- roofline of the dominant kernel (the DMMA GEMM)
+    achieved = gfl.value / (gmsl.value * 1e-3) / 1e12 if gmsl.value > 0 else 0.0
+    f_step = 3 * flops_per_update(d, chi, chi, chi, explicit)
+    roofline = {
+        "bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
+        "frac": achieved / dmma_peak if dmma_peak else None, "traffic": None,
+        "kernel": "zgemm_kernel (mma.sync m8n8k4 f64 -> DMMA, TMA-staged)",
+        "peak_source": "FP64 DMMA microbenchmark (csrc/probe.cu) measured in this run; MEASURED_PEAKS.json has no FP64",
+        "gemm_share_of_step": (gmsl.value / args.steps) / (sum(step_ms) / args.steps),
+        "gemm_launches_per_step": int(gll.value) / args.steps,
+        "step_achieved_tflops": f_step / (ms_per_step * 1e-3) / 1e12,
+        "step_frac": f_step / (ms_per_step * 1e-3) / 1e12 / dmma_peak,
+        "flops_per_step": f_step,
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws, "steps": args.steps, "warmup": warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "complex128", "data": "synthetic",
+        "config": {"workload": desc, "d": d, "chi": chi, "scheme": scheme, "cell_length": 2,
+                   "explicit_error": explicit, "trotter_order": 2, "updates_per_step": 3,
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+                   "l2": "flushed (256 MB write) between timed steps, outside the per-step event pair"},
+        "updates_per_s": 3 * value,
+        "roofline": roofline,
+        "e2e": {"value": ws * 1e3 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, n, dt = cpu_reference_rate(d, chi, scheme, explicit, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"{n} Trotter steps ({dt:.1f} s) of the NumPy/LAPACK oracle on the same "
+                                          f"config, OpenBLAS threads = {os.cpu_count()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

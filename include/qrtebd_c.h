@@ -179,6 +179,11 @@ qt_status qt_bond_energy(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m,
                          const qt_tensor* h_bond, double* out);
 
 /* ---- diagnostics ---------------------------------------------------------- */
+/* Per-launch CUDA-event profile of the DMMA GEMM kernel (roofline evidence):
+ * between begin and end every GEMM launch is bracketed by events; end
+ * synchronizes and returns summed algorithmic flops, device ms and launches. */
+qt_status qt_profile_begin(qt_ctx* ctx);
+qt_status qt_profile_end(qt_ctx* ctx, double* gemm_flops, double* gemm_ms, uint64_t* gemm_launches);
 /* measured FP64 peak of this device in TFLOP/s: kind 0 = DMMA, 1 = DFMA */
 qt_status qt_fp64_peak(qt_ctx* ctx, int kind, double* tflops);
 

@@ -94,6 +94,8 @@ SIGNATURES = {
     "qt_right_defect": (C.c_int, [P, P, DP]),
     "qt_bond_energy": (C.c_int, [P, P, P, P, P, DP]),
     "qt_fp64_peak": (C.c_int, [P, C.c_int, DP]),
+    "qt_profile_begin": (C.c_int, [P]),
+    "qt_profile_end": (C.c_int, [P, DP, DP, U64P]),
 }
 
 _lib = None

@@ -224,7 +224,7 @@ void permute(Engine& e, const double2* in, int rank, const long long* shape, con
     dim3 grid(static_cast<unsigned>(ceil_div(C, 32)), static_cast<unsigned>(ceil_div(R, 32)),
               static_cast<unsigned>(batch));
     transpose_tiled_kernel<<<grid, dim3(32, 8), 0, e.stream>>>(in, R, C, conj, out);
-    QT_CUDA(cudaGetLastError());
+    QT_LAUNCHED();
     return;
   }
   Perm4 p{};
@@ -234,34 +234,34 @@ void permute(Engine& e, const double2* in, int rank, const long long* shape, con
     p.in_stride_for_out[k] = in_strides[perm[k]];
   }
   permute_kernel<<<grid_for(total), 256, 0, e.stream>>>(in, p, total, conj, scale, dscale, out);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
 }
 
 void norm2(Engine& e, const double2* x, long long rows, long long cols, long long ld, double* out) {
   double* part = e.dbuf(S_NORM_PART, kNormBlocks);
   norm2_partial_kernel<<<kNormBlocks, 256, 0, e.stream>>>(x, rows, cols, ld, part);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
   norm2_final_kernel<<<1, 512, 0, e.stream>>>(part, kNormBlocks, out);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
 }
 
 void copy2d(Engine& e, const double2* src, long long lds, double2* dst, long long ldd, long long rows,
             long long cols) {
   if (rows * cols == 0) return;
   copy2d_kernel<<<grid_for(rows * cols), 256, 0, e.stream>>>(src, lds, dst, ldd, rows, cols);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
 }
 
 void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld) {
   if (rows * cols == 0) return;
   identity_kernel<<<grid_for(rows * cols), 256, 0, e.stream>>>(q, rows, cols, ld);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
 }
 
 void check_finite(Engine& e, const double2* x, long long n, int* dflag) {
   if (n == 0) return;
   finite_kernel<<<grid_for(n), 256, 0, e.stream>>>(x, n, dflag);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
 }
 
 }  // namespace qt

@@ -717,6 +717,23 @@ qt_status qt_bond_energy(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m,
   });
 }
 
+qt_status qt_profile_begin(qt_ctx* ctx) {
+  return guard([&] {
+    require(ctx != nullptr, qt::Err::input, "null context");
+    qt::gemm_profile_begin();
+  });
+}
+
+qt_status qt_profile_end(qt_ctx* ctx, double* gemm_flops, double* gemm_ms, uint64_t* gemm_launches) {
+  return guard([&] {
+    require(ctx && gemm_flops && gemm_ms && gemm_launches, qt::Err::input, "null argument");
+    const qt::GemmProfile p = qt::gemm_profile_end();
+    *gemm_flops = p.flops;
+    *gemm_ms = p.ms;
+    *gemm_launches = p.launches;
+  });
+}
+
 qt_status qt_fp64_peak(qt_ctx* ctx, int kind, double* tflops) {
   return guard([&] {
     require(ctx && tflops, qt::Err::input, "qt_fp64_peak: null argument");

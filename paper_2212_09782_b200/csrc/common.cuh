@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -29,6 +30,14 @@ inline void cuda_check(cudaError_t e, const char* what) {
     throw Error(Err::cuda, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define QT_CUDA(x) ::qt::cuda_check((x), #x)
+
+// every kernel launch of the library is counted (bench "gpu_launches")
+inline std::atomic<unsigned long long> g_kernel_launches{0};
+#define QT_LAUNCHED()                                        \
+  do {                                                       \
+    ::qt::cuda_check(cudaGetLastError(), "kernel launch");   \
+    ::qt::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+  } while (0)
 
 constexpr int kNumSMs = 148;
 

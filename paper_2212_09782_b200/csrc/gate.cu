@@ -209,7 +209,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   }
   norm2(e, Rp, eta, eta, eta, e.dscal + SC_L2);
   inv_norm_kernel<<<1, 1, 0, e.stream>>>(e.dscal, SC_THETA2, SC_L2, pol.skip_renormalize ? 1 : 0, SC_TMP0);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
   {
     // Xi~ = L / den = Rp^H / den   (gates.cpp:365-370)
     const long long shp[2] = {eta, eta};
@@ -285,7 +285,7 @@ void expectation_local(Engine& e, const double2* xi, long long chi_l, const doub
   }
   gemm(e, Op::N, Op::H, d, d, chi_l * chi_r, t1, chi_l * chi_r, b, chi_l * chi_r, t2, d);
   trace_op_kernel<<<1, 32, 0, e.stream>>>(op, t2, static_cast<int>(d), e.dscal + SC_TMP1);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
   QT_CUDA(cudaMemcpyAsync(out2_host, e.dscal + SC_TMP1, 2 * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
   QT_CUDA(cudaStreamSynchronize(e.stream));
 }

@@ -251,6 +251,7 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp) {
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
   QT_CUDA(cudaLaunchKernelEx(&cfg, panel_kernel, a));
+  QT_LAUNCHED();
 }
 
 }  // namespace
@@ -344,9 +345,9 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   }
 
   gauge_q_kernel<<<grid_for(m * k), 256, 0, e.stream>>>(a, lda, q, ldq, m, k);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
   gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
-  QT_CUDA(cudaGetLastError());
+  QT_LAUNCHED();
 }
 
 }  // namespace qt

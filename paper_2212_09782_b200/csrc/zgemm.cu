@@ -19,6 +19,7 @@
 #include <atomic>
 #include <cstdio>
 #include <mutex>
+#include <vector>
 
 #include "zgemm.cuh"
 
@@ -26,7 +27,25 @@ namespace qt {
 
 namespace {
 
-std::atomic<unsigned long long> g_launches{0};
+// launch profiler: CUDA events around every DMMA GEMM launch (bench roofline)
+struct Prof {
+  bool active = false;
+  struct Rec {
+    cudaEvent_t e0, e1;
+    double flops;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  cudaEvent_t event() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      QT_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+} g_prof;
 
 // ---------------------------------------------------------------- PTX glue
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -450,21 +469,28 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
 
   dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m),
             static_cast<unsigned>(d.batch * splits));
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (g_prof.active) {
+    ev0 = g_prof.event();
+    ev1 = g_prof.event();
+    QT_CUDA(cudaEventRecord(ev0, st));
+  }
   kern<<<grid, C_::THREADS, C_::SMEM, st>>>(tA, tB, p);
-  QT_CUDA(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  QT_LAUNCHED();
+  if (g_prof.active) {
+    QT_CUDA(cudaEventRecord(ev1, st));
+    g_prof.recs.push_back({ev0, ev1, 8.0 * d.M * d.N * d.K * d.batch});
+  }
   if (MODE == 0 && splits > 1) {
     const long long total = static_cast<long long>(d.batch) * d.M * d.N;
     const int blocks = static_cast<int>(std::min<long long>(ceil_div(total, 256), 8 * kNumSMs));
     splitk_reduce_kernel<<<blocks, 256, 0, st>>>(s.partial, splits, d.batch, d.M, d.N, d.C, d.ldc, d.strideC,
                                                  p.rsplit, d.ldc_hi, d.alpha, d.beta);
-    QT_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    QT_LAUNCHED();
   }
   if (MODE == 1) {
     sum_reduce_kernel<<<1, 256, 0, st>>>(s.tile_sums, tiles_m * tiles_n * d.batch, resid_out);
-    QT_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    QT_LAUNCHED();
   }
 }
 
@@ -502,6 +528,28 @@ void zgemm(const GemmDesc& d, const GemmScratch& s, cudaStream_t stream, double*
     dispatch_ops<1>(d, s, stream, resid_out);
 }
 
-unsigned long long zgemm_launch_count() { return g_launches.load(); }
+unsigned long long zgemm_launch_count() { return g_kernel_launches.load(); }
+
+void gemm_profile_begin() {
+  g_prof.active = true;
+  g_prof.recs.clear();
+  g_prof.next = 0;
+}
+
+GemmProfile gemm_profile_end() {
+  GemmProfile r;
+  g_prof.active = false;
+  for (const auto& rec : g_prof.recs) {
+    QT_CUDA(cudaEventSynchronize(rec.e1));
+    float ms = 0.f;
+    QT_CUDA(cudaEventElapsedTime(&ms, rec.e0, rec.e1));
+    r.ms += ms;
+    r.flops += rec.flops;
+    r.launches += 1;
+  }
+  g_prof.recs.clear();
+  g_prof.next = 0;
+  return r;
+}
 
 }  // namespace qt

@@ -52,7 +52,17 @@ struct GemmScratch {
 void zgemm(const GemmDesc& d, const GemmScratch& s, cudaStream_t stream,
            double* resid_out = nullptr);
 
-// number of DMMA kernels launched since process start (bench bookkeeping)
+// number of library kernels launched since process start (bench bookkeeping)
 unsigned long long zgemm_launch_count();
+
+// GEMM launch profiler: CUDA events around every DMMA GEMM launch between
+// begin and end; end synchronizes and returns the summed algorithmic flops
+// (8 per complex MAC) and device time.
+struct GemmProfile {
+  double flops = 0.0, ms = 0.0;
+  unsigned long long launches = 0;
+};
+void gemm_profile_begin();
+GemmProfile gemm_profile_end();
 
 }  // namespace qt
