@@ -18,6 +18,9 @@
 // I - V T V^H applied with three DMMA GEMMs (V^H A, T^H W, A - V W2).
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "engine.cuh"
 
 namespace qt {
@@ -59,6 +62,7 @@ struct PanelArgs {
   double2* part;   // [2][grid][32] partial sums
   double2* diag;   // [2][32] broadcast of the current diagonal row
   unsigned* bar;   // grid barrier words
+  long long* dbg;  // optional per-column clock64 stamps (CTA 0, thread 0)
 };
 
 __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_kernel(PanelArgs a) {
@@ -219,14 +223,103 @@ __global__ void gauge_r_kernel(const double2* __restrict__ a, long long lda, dou
   }
 }
 
+#include "qr_panel.cuh"
+
 int grid_for(long long total) {
   const long long b = ceil_div(total, 256);
   return static_cast<int>(b < 16LL * kNumSMs ? (b > 0 ? b : 1) : 16LL * kNumSMs);
 }
 
+// returns false when the panel is too tall for one cluster's shared memory
+template <int RPW>
+void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs) {
+  auto kern = panel_cluster_kernel<RPW>;
+  static bool attr = false;
+  if (!attr) {
+    QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(panel_cluster_smem(RPW))));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(cs));
+  cfg.blockDim = dim3(CL_THREADS);
+  cfg.dynamicSmemBytes = panel_cluster_smem(RPW);
+  cfg.stream = e.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = static_cast<unsigned>(cs);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  QT_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  QT_LAUNCHED();
+}
+
+bool launch_panel_cluster(Engine& e, const PanelArgs& base, long long mp) {
+  static int max_cs = -1;
+  if (max_cs < 0) {
+    auto kern = panel_cluster_kernel<CL_MAX_RPW>;
+    QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const size_t smem_max = panel_cluster_smem(CL_MAX_RPW);
+    QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_max)));
+    max_cs = 0;
+    for (int cs : {16, 8}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(CL_THREADS);
+      cfg.dynamicSmemBytes = smem_max;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1) {
+        max_cs = cs;
+        break;
+      }
+      cudaGetLastError();
+    }
+  }
+  if (max_cs == 0) return false;
+  // as many CTAs as the cluster allows (short per-warp row loops), >= 32 rows
+  // each so CTA 0 owns the whole diagonal block
+  static const int cs_cap = std::getenv("QT_PANEL_CS") ? std::atoi(std::getenv("QT_PANEL_CS")) : 16;
+  const long long cs_max = std::min(max_cs, std::max(1, cs_cap));
+  // rows per warp held in registers: smallest instantiation that covers the
+  // panel with <= cs_max CTAs (16 row warps each)
+  const long long need = ceil_div(mp, cs_max * CL_WARPS);
+  int rpw = 0;
+  for (int r : {2, 3, 5, 8, 10, 14, CL_MAX_RPW})
+    if (r >= need) {
+      rpw = r;
+      break;
+    }
+  if (rpw == 0) return false;
+  const long long cs = ceil_div(mp, static_cast<long long>(rpw) * CL_WARPS);
+  PanelArgs a = base;
+  a.rpc = rpw * CL_WARPS;
+  switch (rpw) {
+    case 2: launch_panel_rpw<2>(e, a, cs); break;
+    case 3: launch_panel_rpw<3>(e, a, cs); break;
+    case 5: launch_panel_rpw<5>(e, a, cs); break;
+    case 8: launch_panel_rpw<8>(e, a, cs); break;
+    case 10: launch_panel_rpw<10>(e, a, cs); break;
+    case 14: launch_panel_rpw<14>(e, a, cs); break;
+    default: launch_panel_rpw<CL_MAX_RPW>(e, a, cs); break;
+  }
+  return true;
+}
+
 void launch_panel(Engine& e, const PanelArgs& base, long long mp) {
-  // ~128 rows per CTA, at most one CTA per SM (co-residency for the grid
-  // barrier), at least 32 rows so CTA 0 owns the whole diagonal block
+  if (launch_panel_cluster(e, base, mp)) return;
+  // grid-wide fallback for very tall panels: ~128 rows per CTA, at most one
+  // CTA per SM (co-residency for the grid barrier), at least 32 rows so CTA 0
+  // owns the whole diagonal block
   long long G = std::min<long long>(e.num_sms, std::max<long long>(1, ceil_div(mp, 128)));
   long long rpc = std::max<long long>(NB, ceil_div(mp, G));
   rpc = ceil_div(rpc, 8) * 8;
@@ -275,6 +368,11 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   base.part = part;
   base.diag = part + 2 * kNumSMs * NB;
   base.bar = e.barrier;
+  // QT_PANEL_DEBUG=1: per-column phase timings of the cluster panel (stderr)
+  static const bool dbg_on = std::getenv("QT_PANEL_DEBUG") != nullptr;
+  static long long* dbg_buf = nullptr;
+  if (dbg_on && !dbg_buf) QT_CUDA(cudaMalloc(&dbg_buf, 4 * NB * sizeof(long long)));
+  base.dbg = dbg_on ? dbg_buf : nullptr;
 
   for (long long p = 0; p < npan; ++p) {
     const long long j = p * NB;
@@ -287,6 +385,20 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
     pa.V = V + j * kp + p * NB;
     pa.T = T + p * NB * NB;
     launch_panel(e, pa, mp);
+    if (dbg_on) {
+      long long h[4 * NB];
+      QT_CUDA(cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, e.stream));
+      QT_CUDA(cudaStreamSynchronize(e.stream));
+      double ph[4] = {0, 0, 0, 0};
+      for (int c = 0; c + 1 < nbp; ++c) {
+        ph[0] += h[c * 4 + 1] - h[c * 4 + 0];      // reduce + push
+        ph[1] += h[c * 4 + 2] - h[c * 4 + 1];      // wait for the cluster partials
+        ph[2] += h[c * 4 + 3] - h[c * 4 + 2];      // combine + reflector
+        ph[3] += h[(c + 1) * 4 + 0] - h[c * 4 + 3];  // fused row pass
+      }
+      std::fprintf(stderr, "panel m=%lld nbp=%d cycles/col: push %.0f wait %.0f refl %.0f rows %.0f\n", mp, nbp,
+                   ph[0] / (nbp - 1), ph[1] / (nbp - 1), ph[2] / (nbp - 1), ph[3] / (nbp - 1));
+    }
     const long long ntr = n - j - nbp;
     if (ntr > 0) {
       GemmDesc g;

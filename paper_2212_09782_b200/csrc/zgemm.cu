@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
   // --------------------------------------------------------------- epilogue
   if (MODE == 0) {
     const bool partial_out = p.splits > 1;
+    const bool has_beta = !partial_out && p.beta != 0.0;
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
       const long long row = m0 + wm0 + 8 * i + r8;
@@ -275,8 +276,22 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
       long long rbase;
       if (partial_out)
         rbase = (static_cast<long long>(z) * p.M + row) * p.N;
+      else if (p.rsplit > p.M)
+        rbase = static_cast<long long>(b) * p.strideC + row * p.ldc;
       else
         rbase = static_cast<long long>(b) * p.strideC + (row % p.rsplit) * p.ldc + (row / p.rsplit) * p.ldc_hi;
+      // beta != 0: issue every C load of this row before the first store so
+      // the DRAM/L2 round trips overlap (C aliases the stores)
+      double2 old[NJ][2];
+      if (has_beta) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const long long col = n0 + wn0 + 8 * j + t + 4 * h;
+            old[j][h] = col < p.N ? p.C[rbase + col] : make_double2(0.0, 0.0);
+          }
+      }
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
 #pragma unroll
@@ -289,10 +304,9 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
           } else {
             v.x *= p.alpha;
             v.y *= p.alpha;
-            if (p.beta != 0.0) {
-              const double2 o = p.C[rbase + col];
-              v.x = fma(p.beta, o.x, v.x);
-              v.y = fma(p.beta, o.y, v.y);
+            if (has_beta) {
+              v.x = fma(p.beta, old[j][h].x, v.x);
+              v.y = fma(p.beta, old[j][h].y, v.y);
             }
             p.C[rbase + col] = v;
           }
@@ -496,12 +510,18 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
 
 template <int OPA, int OPB, int MODE>
 void dispatch_shape(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double* r) {
-  // 64x128 tile (8 DMMA warps of 32x32) for everything with >= 64 rows;
-  // 32x128 (4 warps) for the skinny Householder products and gate mixes.
-  if (d.M <= 32)
+  // Largest tile that still fills one wave of 148 SMs; the 32x64 tile (two
+  // CTAs per SM) plus automatic split-K covers the small, latency-bound
+  // products of the chi <= 256 updates and the Householder block reflectors.
+  auto tiles = [&](long long bm, long long bn) { return ceil_div(d.M, bm) * ceil_div(d.N, bn) * d.batch; };
+  if (d.M > 32 && tiles(64, 128) >= kNumSMs)
+    launch_cfg<OPA, OPB, 2, 4, 32, 32, 16, 4, MODE>(d, s, st, r);
+  else if (d.M > 32 && tiles(64, 64) >= kNumSMs)
+    launch_cfg<OPA, OPB, 2, 2, 32, 32, 16, 3, MODE>(d, s, st, r);
+  else if (d.M <= 32 && tiles(32, 128) >= kNumSMs)
     launch_cfg<OPA, OPB, 1, 4, 32, 32, 16, 4, MODE>(d, s, st, r);
   else
-    launch_cfg<OPA, OPB, 2, 4, 32, 32, 16, 4, MODE>(d, s, st, r);
+    launch_cfg<OPA, OPB, 2, 2, 16, 32, 16, 4, MODE>(d, s, st, r);
 }
 
 template <int MODE>
