@@ -171,6 +171,10 @@ qt_status qt_expectation_local(qt_ctx* ctx, const qt_tensor* xi_left, const qt_t
 /* schmidt_values, mps.cpp:198-201: singular values of the bond matrix,
  * descending; out has capacity *n on entry, count on exit. */
 qt_status qt_schmidt_values(qt_ctx* ctx, const qt_tensor* xi, double* out, uint64_t* n);
+/* eigh, proj/src/linalg.cpp:79-101: Hermitian (symmetrized) n x n matrix ->
+ * eigenvalues descending (host array of n) and eigenvectors as the columns of
+ * a new n x n device tensor (device block-Jacobi solver). */
+qt_status qt_eigh(qt_ctx* ctx, const qt_tensor* h, double* w_host, qt_tensor** v_out);
 /* right_defect, mps.cpp:34-36: || sum_i B^i B^i^H - 1 ||_max */
 qt_status qt_right_defect(qt_ctx* ctx, const qt_tensor* b, double* out);
 /* Bond energy <theta0|h|theta0>/<theta0|theta0>, theta0 = Xi B^m B^n

@@ -92,6 +92,7 @@ SIGNATURES = {
     "qt_expectation_local": (C.c_int, [P, P, P, P, DP]),
     "qt_schmidt_values": (C.c_int, [P, P, DP, U64P]),
     "qt_right_defect": (C.c_int, [P, P, DP]),
+    "qt_eigh": (C.c_int, [P, P, DP, PP]),
     "qt_bond_energy": (C.c_int, [P, P, P, P, P, DP]),
     "qt_fp64_peak": (C.c_int, [P, C.c_int, DP]),
     "qt_profile_begin": (C.c_int, [P]),

@@ -561,7 +561,7 @@ qt_status qt_tebd_step_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* con
     };
     std::vector<Pending> pend;
     std::vector<qt_report> reps;
-    double* rep_dev = ctx->eng.dbuf(qt::S_GRAM, 4 * (n_layers * (L / 2 + 1) + 1));
+    double* rep_dev = ctx->eng.dbuf(qt::S_REPORTS, 4 * (n_layers * (L / 2 + 1) + 1));
     for (uint64_t l = 0; l < n_layers; ++l) {
       const qt_tensor* u = gates[l];
       require_gate(u, d);
@@ -692,11 +692,31 @@ qt_status qt_schmidt_values(qt_ctx* ctx, const qt_tensor* xi, double* out, uint6
     qt::Engine& e = ctx->eng;
     const long long p = xi->shape[0], q = xi->shape[1], k = std::min(p, q);
     require(static_cast<uint64_t>(k) <= *n, qt::Err::capacity, "qt_schmidt_values: output too small");
-    double* s = e.dbuf(qt::S_EIG_W, k + 1);
-    qt::singular_values_device(e, xi->data, p, q, s);
+    const double* s = qt::singular_values_device(e, xi->data, p, q);
     QT_CUDA(cudaMemcpyAsync(out, s, k * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
     QT_CUDA(cudaStreamSynchronize(e.stream));
     *n = k;
+  });
+}
+
+qt_status qt_eigh(qt_ctx* ctx, const qt_tensor* h, double* w_host, qt_tensor** v_out) {
+  return guard([&] {
+    require(ctx && h && w_host && v_out, qt::Err::input, "qt_eigh: null argument");
+    require_tensor(h, 2, "eigh");
+    if (h->shape[0] != h->shape[1]) throw qt::Error(qt::Err::shape, "eigh: matrix not square");
+    qt::Engine& e = ctx->eng;
+    const long long n = h->shape[0];
+    qt_tensor* v = new_tensor(ctx, {static_cast<uint64_t>(n), static_cast<uint64_t>(n)});
+    try {
+      double* w = e.dbuf(qt::S_EIG_W, n + 8);
+      qt::eigh_device(e, h->data, n, w, v->data);
+      QT_CUDA(cudaMemcpyAsync(w_host, w, n * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+      QT_CUDA(cudaStreamSynchronize(e.stream));
+    } catch (...) {
+      free_tensor(v);
+      throw;
+    }
+    *v_out = v;
   });
 }
 

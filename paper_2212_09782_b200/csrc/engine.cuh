@@ -36,6 +36,7 @@ enum Slot : int {
   S_EIG_W,
   S_MISC,
   S_MISC2,
+  S_REPORTS,
   S_COUNT
 };
 

@@ -62,8 +62,9 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
 // eigh of a Hermitian n x n matrix on the device (proj/src/linalg.cpp:79-101):
 // eigenvalues descending into w (device), eigenvectors as columns of v (device, ld n)
 void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v);
-// singular values of an arbitrary p x q matrix, descending (device out, min(p,q))
-void singular_values_device(Engine& e, const double2* m, long long p, long long q, double* s);
+// singular values of an arbitrary p x q matrix, descending; returns a device
+// pointer (engine slot S_EIG_W) to min(p,q) values
+double* singular_values_device(Engine& e, const double2* m, long long p, long long q);
 
 // observables (proj/src/mps.cpp)
 void expectation_local(Engine& e, const double2* xi, long long chi_l, const double2* b, long long d,

@@ -1,0 +1,435 @@
+// K5/K9: Hermitian eigensolver on the device (block two-sided Jacobi).
+//
+// Replaces eigh (proj/src/linalg.cpp:79-101: Eigen SelfAdjointEigenSolver on
+// the symmetrized matrix, eigenpairs re-sorted descending) for the CBE Gram
+// matrix G = L^H L (proj/src/gates.cpp:408-413) and for the Schmidt spectra of
+// the bond matrices (singular values via the Gram matrix).
+//
+// One persistent cooperative kernel per solve.  The matrix is padded to N =
+// 16 * nb (nb even) with decoupled diagonal entries below every eigenvalue.
+// Each sweep runs nb-1 rounds of a round-robin pairing of 16-wide blocks; a
+// round is
+//   A. one CTA per block pair (I,J): load the 32x32 Hermitian subproblem
+//      G[X,X], X = I u J, run one inner cyclic Jacobi sweep in shared memory
+//      (31 rounds x 16 disjoint complex rotations) and store its unitary J_X;
+//   B. every 32x32 tile G[X,Y] <- J_X^H G[X,Y] J_Y and every row chunk
+//      V[r,Y] <- V[r,Y] J_Y.
+// Sweeps stop when no rotation in a full sweep met an off-diagonal element
+// above tol = 1e-16 ||G||_F (absolute accuracy of LAPACK's zheevd), at most
+// 30 sweeps.  Every reduction has a fixed order: results are bitwise
+// reproducible run to run.
+#include <cstdio>
+
+#include "gate.cuh"
+
+namespace qt {
+namespace {
+
+constexpr int JB = 16;       // block width
+constexpr int JX = 2 * JB;   // subproblem size
+constexpr int JT = 256;      // threads per CTA
+constexpr int MAX_SWEEPS = 30;
+
+__device__ __forceinline__ void jgrid_sync(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// block (or local index) at position j of round r of a round-robin over n slots
+__device__ __forceinline__ int rr_slot(int j, int r, int n) { return j == 0 ? 0 : 1 + (j - 1 + r) % (n - 1); }
+
+struct JacobiArgs {
+  double2* G;     // N x N, row-major
+  double2* V;     // N x N
+  double2* Jbuf;  // [npairs][32][32]
+  double* flags;  // [MAX_SWEEPS] per-sweep max |offdiag| (reduced per CTA into slots below)
+  double* cta_max;  // [gridDim][2]
+  unsigned* bar;
+  int N, nb;
+  double tol;
+  int* sweeps_out;
+};
+
+// complex Jacobi rotation for [[a, c], [c*, b]] (a, b real): U = [[cs, sn],
+// [-sn e^{-i phi}, cs e^{-i phi}]] zeroes the off-diagonal of U^H A U
+struct Rot {
+  double cs, sn;
+  double2 e;  // e^{-i phi}
+  bool active;
+};
+
+// off-diagonal size relative to the diagonal pair (Demmel-Veselic): rotating
+// whenever |c| > eps sqrt(|a b|) keeps the small eigenvalues of graded PSD
+// Gram matrices (the CBE spectrum) accurate to high relative precision
+__device__ __forceinline__ double rel_off(double a, double b, double2 c) {
+  const double ac = hypot(c.x, c.y);
+  const double sc = sqrt(fabs(a) * fabs(b));
+  return ac == 0.0 ? 0.0 : (sc > 0.0 ? ac / sc : INFINITY);
+}
+
+__device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double tol) {
+  Rot r;
+  const double ac = hypot(c.x, c.y);
+  r.active = rel_off(a, b, c) > tol && ac > 1e-300;
+  if (!r.active) {
+    r.cs = 1.0;
+    r.sn = 0.0;
+    r.e = make_double2(1.0, 0.0);
+    return r;
+  }
+  r.e = make_double2(c.x / ac, -c.y / ac);
+  const double theta = (b - a) / (2.0 * ac);
+  const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+  r.cs = 1.0 / sqrt(t * t + 1.0);
+  r.sn = t * r.cs;
+  return r;
+}
+
+__global__ void __launch_bounds__(JT) jacobi_kernel(JacobiArgs a) {
+  extern __shared__ double2 jdyn[];
+  double2(*S)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn);
+  double2(*Jm)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn + JX * (JX + 1));
+  double2(*T1)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn + 2 * JX * (JX + 1));
+  __shared__ Rot rots[JX / 2];
+  __shared__ int rp[JX / 2], rq[JX / 2];
+  __shared__ double red[JT];
+  __shared__ int done_flag;
+
+  const int tid = threadIdx.x;
+  const unsigned G = gridDim.x;
+  const int npairs = a.nb / 2;
+  const int N = a.N;
+  int sweep = 0;
+
+  for (; sweep < MAX_SWEEPS; ++sweep) {
+    double mx = 0.0;  // max |offdiag| met by this CTA during the sweep
+    for (int round = 0; round < a.nb - 1; ++round) {
+      // ---------------- phase A: 32x32 subproblems
+      for (int p = blockIdx.x; p < npairs; p += G) {
+        const int bI = rr_slot(p, round, a.nb), bJ = rr_slot(a.nb - 1 - p, round, a.nb);
+        // local index l < 16 -> bI*16 + l, else bJ*16 + l - 16
+        for (int e = tid; e < JX * JX; e += JT) {
+          const int i = e / JX, j = e % JX;
+          const int gi = (i < JB ? bI * JB + i : bJ * JB + i - JB);
+          const int gj = (j < JB ? bI * JB + j : bJ * JB + j - JB);
+          S[i][j] = a.G[static_cast<long long>(gi) * N + gj];
+          Jm[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+        }
+        __syncthreads();
+        for (int ir = 0; ir < JX - 1; ++ir) {
+          if (tid < JX / 2) {
+            int p0 = rr_slot(tid, ir, JX), q0 = rr_slot(JX - 1 - tid, ir, JX);
+            if (p0 > q0) {
+              const int tmp = p0;
+              p0 = q0;
+              q0 = tmp;
+            }
+            rp[tid] = p0;
+            rq[tid] = q0;
+            const double2 c = S[p0][q0];
+            const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, c, a.tol);
+            if (rr.active) mx = fmax(mx, rel_off(S[p0][p0].x, S[q0][q0].x, c));
+            rots[tid] = rr;
+          }
+          __syncthreads();
+          // rows: S[p,:] <- cs S[p,:] - sn conj(e) S[q,:];  S[q,:] <- sn S[p,:] + cs conj(e) S[q,:]
+          for (int e = tid; e < (JX / 2) * JX; e += JT) {
+            const int k = e / JX, j = e % JX;
+            const Rot r = rots[k];
+            if (!r.active) continue;
+            const int p0 = rp[k], q0 = rq[k];
+            const double2 sp = S[p0][j], sq = S[q0][j];
+            const double2 ce = cconj(r.e);
+            S[p0][j] = csub(cscale(sp, r.cs), cscale(cmul(ce, sq), r.sn));
+            S[q0][j] = cadd(cscale(sp, r.sn), cscale(cmul(ce, sq), r.cs));
+          }
+          __syncthreads();
+          // columns of S and of J: X[:,p] <- cs X[:,p] - sn e X[:,q];  X[:,q] <- sn X[:,p] + cs e X[:,q]
+          for (int e = tid; e < (JX / 2) * JX * 2; e += JT) {
+            const int which = e / ((JX / 2) * JX);
+            const int ee = e % ((JX / 2) * JX);
+            const int k = ee / JX, i = ee % JX;
+            const Rot r = rots[k];
+            if (!r.active) continue;
+            const int p0 = rp[k], q0 = rq[k];
+            double2(*X)[JX + 1] = which == 0 ? S : Jm;
+            const double2 xp = X[i][p0], xq = X[i][q0];
+            X[i][p0] = csub(cscale(xp, r.cs), cscale(cmul(r.e, xq), r.sn));
+            X[i][q0] = cadd(cscale(xp, r.sn), cscale(cmul(r.e, xq), r.cs));
+          }
+          __syncthreads();
+        }
+        for (int e = tid; e < JX * JX; e += JT) a.Jbuf[static_cast<long long>(p) * JX * JX + e] = Jm[e / JX][e % JX];
+        __syncthreads();
+      }
+      jgrid_sync(a.bar, G);
+      // ---------------- phase B: tile updates of G and V
+      const int nrowchunks = N / JX;
+      const int ntiles = npairs * npairs + nrowchunks * npairs;
+      for (int t = blockIdx.x; t < ntiles; t += G) {
+        const bool isG = t < npairs * npairs;
+        int xa, yb, rc = 0;
+        if (isG) {
+          xa = t / npairs;
+          yb = t % npairs;
+        } else {
+          const int u = t - npairs * npairs;
+          rc = u / npairs;
+          yb = u % npairs;
+          xa = -1;
+        }
+        const int yI = rr_slot(yb, round, a.nb), yJ = rr_slot(a.nb - 1 - yb, round, a.nb);
+        int xI = 0, xJ = 0;
+        if (isG) {
+          xI = rr_slot(xa, round, a.nb);
+          xJ = rr_slot(a.nb - 1 - xa, round, a.nb);
+        }
+        double2* M = isG ? a.G : a.V;
+        // load tile into S, J_Y into Jm
+        for (int e = tid; e < JX * JX; e += JT) {
+          const int i = e / JX, j = e % JX;
+          const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
+          const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
+          S[i][j] = M[static_cast<long long>(gi) * N + gj];
+          Jm[i][j] = a.Jbuf[static_cast<long long>(yb) * JX * JX + e];
+        }
+        __syncthreads();
+        // T1 = S Jy
+        for (int e = tid; e < JX * JX; e += JT) {
+          const int i = e / JX, j = e % JX;
+          double2 s = make_double2(0.0, 0.0);
+#pragma unroll 8
+          for (int l = 0; l < JX; ++l) s = cadd(s, cmul(S[i][l], Jm[l][j]));
+          T1[i][j] = s;
+        }
+        __syncthreads();
+        if (isG) {
+          // out = Jx^H T1
+          for (int e = tid; e < JX * JX; e += JT) Jm[e / JX][e % JX] = a.Jbuf[static_cast<long long>(xa) * JX * JX + e];
+          __syncthreads();
+          for (int e = tid; e < JX * JX; e += JT) {
+            const int i = e / JX, j = e % JX;
+            double2 s = make_double2(0.0, 0.0);
+#pragma unroll 8
+            for (int l = 0; l < JX; ++l) s = cadd(s, cmul(cconj(Jm[l][i]), T1[l][j]));
+            S[i][j] = s;
+          }
+          __syncthreads();
+        }
+        double2(*O)[JX + 1] = isG ? S : T1;
+        for (int e = tid; e < JX * JX; e += JT) {
+          const int i = e / JX, j = e % JX;
+          const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
+          const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
+          M[static_cast<long long>(gi) * N + gj] = O[i][j];
+        }
+        __syncthreads();
+      }
+      jgrid_sync(a.bar, G);
+    }
+    // ---------------- convergence: max over CTAs of the largest rotated element
+    red[tid] = mx;
+    __syncthreads();
+    for (int w = JT / 2; w > 0; w >>= 1) {
+      if (tid < w) red[tid] = fmax(red[tid], red[tid + w]);
+      __syncthreads();
+    }
+    if (tid == 0) a.cta_max[(sweep & 1) * G + blockIdx.x] = red[0];
+    jgrid_sync(a.bar, G);
+    if (tid == 0) {
+      double m = 0.0;
+      for (unsigned b = 0; b < G; ++b) m = fmax(m, __ldcg(&a.cta_max[(sweep & 1) * G + b]));
+      done_flag = m <= a.tol;
+    }
+    __syncthreads();
+    if (done_flag) break;
+  }
+  if (blockIdx.x == 0 && tid == 0) *a.sweeps_out = sweep + 1;
+}
+
+// pad: G_pad = [[G, 0], [0, diag(-(|G|+1) - i)]], V = I
+__global__ void jacobi_setup_kernel(const double2* __restrict__ h, int n, int N, const double* fro, double2* G,
+                                    double2* V) {
+  const double shift = -(sqrt(*fro) + 1.0);
+  const long long total = static_cast<long long>(N) * N;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / N), j = static_cast<int>(e % N);
+    double2 g = make_double2(0.0, 0.0);
+    if (i < n && j < n) {
+      // symmetrize (proj/src/linalg.cpp:87): 0.5 (h + h^H)
+      const double2 x = h[static_cast<long long>(i) * n + j], y = h[static_cast<long long>(j) * n + i];
+      g = make_double2(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+      if (i == j) g.y = 0.0;
+    } else if (i == j) {
+      g = make_double2(shift - i, 0.0);
+    }
+    G[e] = g;
+    V[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+}
+
+// sort the N diagonal entries descending (ties: lower index first), write the
+// first n eigenvalues and the matching eigenvector columns (n x n, ld n)
+__global__ void jacobi_sort_kernel(const double2* __restrict__ G, const double2* __restrict__ V, int n, int N,
+                                   double* w, double2* vout) {
+  extern __shared__ unsigned char jsm[];
+  int P = 1;
+  while (P < N) P <<= 1;
+  double* k2 = reinterpret_cast<double*>(jsm);  // capacity P
+  int* idx = reinterpret_cast<int*>(k2 + P);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    k2[i] = i < N ? G[static_cast<long long>(i) * N + i].x : -INFINITY;
+    idx[i] = i;
+  }
+  __syncthreads();
+  // bitonic sort, descending by key, ascending by index on ties
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          const bool i_first = (k2[i] > k2[j]) || (k2[i] == k2[j] && idx[i] < idx[j]);
+          if (desc != i_first) {
+            const double tk = k2[i];
+            k2[i] = k2[j];
+            k2[j] = tk;
+            const int ti = idx[i];
+            idx[i] = idx[j];
+            idx[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = k2[i];
+  for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += blockDim.x) {
+    const int r = static_cast<int>(e / n), c = static_cast<int>(e % n);
+    vout[e] = V[static_cast<long long>(r) * N + idx[c]];
+  }
+}
+
+__global__ void sqrt_clip_kernel(const double* __restrict__ w, int n, double* s) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    s[i] = w[i] > 0.0 ? sqrt(w[i]) : 0.0;
+}
+
+}  // namespace
+
+void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v) {
+  if (n <= 0) return;
+  int nb = static_cast<int>(ceil_div(n, JB));
+  if (nb < 2) nb = 2;
+  if (nb & 1) ++nb;
+  const int N = nb * JB;
+  const int npairs = nb / 2;
+  double2* G = e.cbuf(S_EIG_V, static_cast<size_t>(2) * N * N + static_cast<size_t>(npairs) * JX * JX);
+  double2* V = G + static_cast<size_t>(N) * N;
+  double2* Jbuf = V + static_cast<size_t>(N) * N;
+  double* fro = e.dscal + SC_TMP2;
+  norm2(e, h, n, n, n, fro);
+  jacobi_setup_kernel<<<static_cast<int>(std::min<long long>(ceil_div(static_cast<long long>(N) * N, 256), 2048)), 256,
+                        0, e.stream>>>(h, static_cast<int>(n), N, fro, G, V);
+  QT_LAUNCHED();
+  const int grid = std::min(e.num_sms, std::max(npairs, std::min(npairs * npairs + (N / JX) * npairs, e.num_sms)));
+  double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8);
+  int* sweeps = reinterpret_cast<int*>(cta_max + 2 * grid);
+  JacobiArgs a;
+  a.G = G;
+  a.V = V;
+  a.Jbuf = Jbuf;
+  a.flags = nullptr;
+  a.cta_max = cta_max;
+  a.bar = e.barrier + 8;
+  a.N = N;
+  a.nb = nb;
+  a.tol = 2.220446049250313e-16;  // relative off-diagonal threshold (unit roundoff)
+  a.sweeps_out = sweeps;
+  const size_t jsmem = 3 * JX * (JX + 1) * sizeof(double2);
+  static bool jattr = false;
+  if (!jattr) {
+    QT_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(jsmem)));
+    jattr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(JT);
+  cfg.dynamicSmemBytes = jsmem;
+  cfg.stream = e.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  QT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel, a));
+  QT_LAUNCHED();
+  int P = 1;
+  while (P < N) P <<= 1;
+  const size_t smem = static_cast<size_t>(P) * (sizeof(double) + sizeof(int));
+  if (smem > 200 * 1024) throw Error(Err::capacity, "eigh: matrix too large for the device sort");
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    QT_CUDA(cudaFuncSetAttribute(jacobi_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    attr = smem;
+  }
+  jacobi_sort_kernel<<<1, 1024, smem, e.stream>>>(G, V, static_cast<int>(n), N, w, v);
+  QT_LAUNCHED();
+}
+
+double* singular_values_device(Engine& e, const double2* m, long long p, long long q) {
+  // s = sqrt(max(eig(m^H m), 0)) (Gram route, absolute accuracy ~ sqrt(u) s_0
+  // for the smallest values), descending; returned in the S_EIG_W slot
+  const long long k = std::min(p, q);
+  if (k == 0) return e.dbuf(S_EIG_W, 8);
+  const bool wide = q > p;  // Gram on the smaller side
+  const long long g = wide ? p : q;
+  double2* gm = e.cbuf(S_GRAM, g * g);
+  GemmDesc d;
+  d.M = g;
+  d.N = g;
+  d.K = wide ? q : p;
+  if (wide) {
+    d.opA = Op::N;  // m m^H
+    d.A = m;
+    d.lda = q;
+    d.opB = Op::H;
+    d.B = m;
+    d.ldb = q;
+  } else {
+    d.opA = Op::H;  // m^H m
+    d.A = m;
+    d.lda = q;
+    d.opB = Op::N;
+    d.B = m;
+    d.ldb = q;
+  }
+  d.C = gm;
+  d.ldc = g;
+  zgemm(d, e.gemm_scratch(), e.stream);
+  double* w = e.dbuf(S_EIG_W, g + 8);
+  double2* v = e.cbuf(S_MISC2, g * g);
+  eigh_device(e, gm, g, w, v);
+  sqrt_clip_kernel<<<1, 256, 0, e.stream>>>(w, static_cast<int>(k), w);
+  QT_LAUNCHED();
+  return w;
+}
+
+}  // namespace qt

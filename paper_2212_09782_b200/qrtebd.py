@@ -308,3 +308,14 @@ def bond_energy(xi, b_m, b_n, h_bond, ctx: Context = None) -> float:
     out = C.c_double()
     check(ctx.lib.qt_bond_energy(ctx.h, *(t.h for t in ts), C.byref(out)))
     return out.value
+
+
+def eigh(h, ctx: Context = None):
+    """eigh, proj/src/linalg.cpp:79-101 (device block Jacobi): (w desc, V device)."""
+    ctx = ctx or default_context()
+    t = _dev(ctx, h)
+    n = t.shape[0]
+    w = (C.c_double * max(1, n))()
+    v = C.c_void_p()
+    check(ctx.lib.qt_eigh(ctx.h, t.h, w, C.byref(v)))
+    return np.array(w[:n]), DeviceTensor(ctx, v)
