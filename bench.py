@@ -43,21 +43,47 @@ sys.path.insert(0, ROOT)
 METRIC = "Trotter steps/sec (2-site QR updates/sec) vs chi,d; FP64 tensor-pipe % of peak"
 
 CONFIGS = {
-    # name: (description, d, chi, scheme, explicit, L)
-    "c1": ("C1 iTEBD transverse-field Ising (clock d=2), L=2, chi=64, qr", 2, 64, "qr", True),
-    "c2": ("C2 clock-model quench d=5, chi=256, uniform L=2, qr (eta=chi), explicit error on", 5, 256, "qr", True),
+    # name: (description, d, chi, scheme, explicit error, (delta_chi_abs, delta_chi_rel))
+    "c1": ("C1 iTEBD transverse-field Ising (clock d=2), L=2, chi=64, qr", 2, 64, "qr", True, (0, 0.0)),
+    "c2": ("C2 clock-model quench d=5, chi=256, uniform L=2, qr (eta=chi), explicit error on", 5, 256, "qr", True,
+           (0, 0.0)),
+    "c2cbe": ("C2 clock-model quench d=5, chi=256, uniform L=2, qr_cbe (eta=356 -> 256), explicit error on", 5, 256,
+              "qr_cbe", True, (100, 0.1)),
     "north": ("north-star clock quench d=5, chi=1024, uniform L=2, qr (eta=chi), explicit error on", 5, 1024, "qr",
-              True),
-    "c3": ("C3 clock d=10, chi=1024, uniform L=2, qr (eta=chi), explicit error on", 10, 1024, "qr", True),
+              True, (0, 0.0)),
+    "northcbe": ("north-star clock quench d=5, chi=1024, uniform L=2, qr_cbe (eta=1127 -> 1024), explicit on", 5,
+                 1024, "qr_cbe", True, (100, 0.1)),
+    "c3": ("C3 clock d=10, chi=1024, uniform L=2, qr_cbe (eta=1127 -> 1024), explicit error on", 10, 1024, "qr_cbe",
+           True, (100, 0.1)),
+    "c4": ("C4 single-bond stress d=5, chi=4096, qr bench cell (eta=chi, explicit off), 3 updates per step", 5, 4096,
+           "qr", False, (0, 0.0)),
 }
 
 
-def flops_per_update(d, chi, eta, kk, explicit):
-    """8 flops per complex MAC."""
+def policy_kw(cfg):
+    _, d, chi, scheme, explicit, (dabs, drel) = cfg
+    return dict(chi_max=chi, delta_chi_abs=dabs, delta_chi_rel=drel, compute_explicit_error=explicit)
+
+
+def widths(cfg):
+    """(eta, kk) of the steady-state update (gates.cpp:94-101, :354-355, :398-419)."""
+    _, d, chi, scheme, _, (dabs, drel) = cfg
+    eta = min(d * chi, chi + max(dabs, math.ceil(drel * chi)))
+    if scheme == "qr":
+        eta = min(eta, chi)
+    return eta, chi
+
+
+def flops_per_update(d, chi, eta, kk, explicit, cbe=False):
+    """8 flops per complex MAC; eigh excluded for CBE."""
     f = 8.0 * (2 * d * d * chi ** 3 + d ** 4 * chi ** 2 + 2 * d * d * chi * chi * eta + d * d * chi * chi * kk)
     f += 2.0 * (16.0 * (d * chi) * eta * eta - 16.0 / 3.0 * eta ** 3)
     if explicit:
         f += 8.0 * (eta * eta * d * chi + d * d * chi * chi * eta)
+    if cbe:
+        f += 8.0 * (eta ** 3 + kk * eta * d * chi)
+        if explicit:
+            f += 8.0 * (eta * eta * kk + eta ** 3)
     return f
 
 
@@ -169,14 +195,15 @@ def barrier(ws):
         dist.barrier()
 
 
-def cpu_reference_rate(d, chi, scheme, explicit, budget_s, min_steps=1, warmup=0, seed=0x51AB):
+def cpu_reference_rate(cfg, budget_s, min_steps=1, warmup=0, seed=0x51AB):
     """Reference algorithm on the host cores: the oracle port (test infra)."""
     from oracle import qrtebd_oracle as ref
     from paper_2212_09782_b200 import model
+    _, d, chi, scheme, _, _ = cfg
     sites, bonds = synthetic_state(d, chi, seed)
     st = ref.UniformMPS(d, [s.copy() for s in sites], [b.copy() for b in bonds])
     sched = [(p, model.make_gate(model.bond_hamiltonian(d, 2.0), dte)) for p, dte in model.layer_structure(0.05, 2)]
-    pol = ref.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=explicit)
+    pol = ref.TruncationPolicy(**policy_kw(cfg))
     for _ in range(warmup):
         st, _ = ref.tebd_step_uniform(st, sched, scheme, pol)
     n, t0 = 0, time.perf_counter()
@@ -193,10 +220,9 @@ def run_reference(args, cfg):
     ws, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
     if rank != 0:
         return 0
-    desc, d, chi, scheme, explicit = cfg
+    desc, d, chi, scheme, explicit, _ = cfg
     # each "step" is a bounded sample: one full Trotter step of the oracle
-    rate, n, dt = cpu_reference_rate(d, chi, scheme, explicit, budget_s=0.0, min_steps=max(1, args.steps),
-                                     warmup=min(args.warmup, 1))
+    rate, n, dt = cpu_reference_rate(cfg, budget_s=0.0, min_steps=max(1, args.steps), warmup=min(args.warmup, 1))
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
@@ -221,6 +247,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--path", default="graph", choices=["graph", "value"],
+                    help="graph: device-resident state, CUDA-graph step; value: C-ABI tebd_step (new handles)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -231,7 +259,7 @@ def main():
     from paper_2212_09782_b200 import qrtebd as q
 
     ws, rank, local = dist_setup()
-    desc, d, chi, scheme, explicit = cfg
+    desc, d, chi, scheme, explicit, _ = cfg
     warmup = max(3, args.warmup)
     ctx = _capi.Context(local)
     lib = ctx.lib
@@ -242,13 +270,39 @@ def main():
     state0 = q.UniformMPS.from_numpy(ctx, d, sites_h, bonds_h)
     sched_h = [(p, model.make_gate(model.bond_hamiltonian(d, 2.0), dte)) for p, dte in model.layer_structure(0.05, 2)]
     sched = [(p, ctx.tensor(u)) for p, u in sched_h]
-    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=explicit)
+    pol = q.TruncationPolicy(**policy_kw(cfg))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > 126 MB L2
 
-    state = state0
-    for _ in range(warmup):
-        state, reps = q.tebd_step(state, sched, scheme, pol, ctx)
+    # The fast path: state resident in HBM (qt_uniform_*), each step one CUDA
+    # graph replay once the bond dimensions are stationary.  --path value
+    # times the value-semantics C-ABI tebd_step instead (new handles per step).
+    graph_path = args.path == "graph"
+    # roofline evidence: CUDA-event pairs around the hot-path contraction GEMMs
+    # (>= 0.5% of an update's flops; the small Householder block-reflector
+    # products stay un-instrumented so the captured step graph stays lean)
+    eta_cfg, kk_cfg = widths(cfg)
+    prof_min_flops = 0.005 * flops_per_update(d, chi, eta_cfg, kk_cfg, explicit, cbe=(scheme == "qr_cbe"))
+    if graph_path:
+        # capture the step graphs with the GEMM event nodes in them (profiling
+        # on); warm-up >= 4 so both buffer-parity graphs exist before timing
+        warmup = max(warmup, 4)
+        if not os.environ.get("QT_BENCH_NO_GRAPH_PROF"):
+            _capi.check(lib.qt_profile_begin(ctx.h, prof_min_flops))
+        dev = q.DeviceUniformMPS(state0, ctx)
+        for _ in range(warmup):
+            reps = dev.step(sched, scheme, pol)
+    else:
+        state = state0
+        for _ in range(warmup):
+            state, reps = q.tebd_step(state, sched, scheme, pol, ctx)
     assert all(r.report.chi_after == chi for r in reps)
+
+    def one_step():
+        nonlocal state
+        if graph_path:
+            return dev.step(sched, scheme, pol)
+        state, r = q.tebd_step(state, sched, scheme, pol, ctx)
+        return r
 
     # ---------------- timed region: device-resident state
     sampler = ClockSampler(local)
@@ -257,13 +311,13 @@ def main():
     torch.cuda.synchronize()
     ctx.synchronize()
     launches0 = lib.qt_kernel_launches()
-    _capi.check(lib.qt_profile_begin(ctx.h))
+    _capi.check(lib.qt_profile_begin(ctx.h, prof_min_flops))
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for k in range(args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()  # L2 flush between timed steps, outside the event pair
         evs[k][0].record(stream)
-        state, reps = q.tebd_step(state, sched, scheme, pol, ctx)
+        reps = one_step()
         evs[k][1].record(stream)
     ctx.synchronize()
     gf, gms, gl = (np.zeros(1), np.zeros(1), np.zeros(1, dtype=np.uint64))
@@ -288,12 +342,22 @@ def main():
     ctx.synchronize()
     e0.record(stream)
     for k in range(args.steps):
-        for t, hbuf in zip(dev_in, flat_in):
-            _capi.check(lib.qt_tensor_upload_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
-        st_in = q.UniformMPS(d, dev_in[:2], dev_in[2:])
-        st_out, _ = q.tebd_step(st_in, sched, scheme, pol, ctx)
-        for t, hbuf in zip(st_out.site_tensors + st_out.bond_matrices, outs_pinned):
-            _capi.check(lib.qt_tensor_download_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
+        if graph_path:
+            # host state -> live device buffers, step, live buffers -> host
+            views = [dev.view("site", m) for m in range(2)] + [dev.view("bond", m) for m in range(2)]
+            for t, hbuf in zip(views, flat_in):
+                _capi.check(lib.qt_tensor_upload_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
+            dev.step(sched, scheme, pol)
+            views = [dev.view("site", m) for m in range(2)] + [dev.view("bond", m) for m in range(2)]
+            for t, hbuf in zip(views, outs_pinned):
+                _capi.check(lib.qt_tensor_download_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
+        else:
+            for t, hbuf in zip(dev_in, flat_in):
+                _capi.check(lib.qt_tensor_upload_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
+            st_in = q.UniformMPS(d, dev_in[:2], dev_in[2:])
+            st_out, _ = q.tebd_step(st_in, sched, scheme, pol, ctx)
+            for t, hbuf in zip(st_out.site_tensors + st_out.bond_matrices, outs_pinned):
+                _capi.check(lib.qt_tensor_download_async(t.h, _capi.C.cast(hbuf.data_ptr(), _capi.DP)))
     e1.record(stream)
     ctx.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws) / args.steps
@@ -301,11 +365,13 @@ def main():
 
     # ---------------- roofline of the dominant kernel (the DMMA GEMM)
     achieved = gfl.value / (gmsl.value * 1e-3) / 1e12 if gmsl.value > 0 else 0.0
-    f_step = 3 * flops_per_update(d, chi, chi, chi, explicit)
+    eta, kk = widths(cfg)
+    f_step = 3 * flops_per_update(d, chi, eta, kk, explicit, cbe=(scheme == "qr_cbe"))
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
         "frac": achieved / dmma_peak if dmma_peak else None, "traffic": None,
-        "kernel": "zgemm_kernel (mma.sync m8n8k4 f64 -> DMMA, TMA-staged)",
+        "kernel": "zgemm_kernel (mma.sync m8n8k4 f64 -> DMMA, TMA-staged): the hot-path contraction launches "
+                  f"(>= {prof_min_flops:.3g} flops each: theta build, projections, Hastings, explicit error)",
         "peak_source": "FP64 DMMA microbenchmark (csrc/probe.cu) measured in this run; MEASURED_PEAKS.json has no FP64",
         "gemm_share_of_step": (gmsl.value / args.steps) / (sum(step_ms) / args.steps),
         "gemm_launches_per_step": int(gll.value) / args.steps,
@@ -321,20 +387,25 @@ def main():
         "config": {"workload": desc, "d": d, "chi": chi, "scheme": scheme, "cell_length": 2,
                    "explicit_error": explicit, "trotter_order": 2, "updates_per_step": 3,
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+                   "path": ("device-resident state, one CUDA graph replay per step (qt_uniform_step)"
+                            if graph_path else "C-ABI qt_tebd_step_uniform, new handles per step"),
                    "l2": "flushed (256 MB write) between timed steps, outside the per-step event pair"},
         "updates_per_s": 3 * value,
+        "step_ms": [round(x, 3) for x in step_ms],
         "roofline": roofline,
         "e2e": {"value": ws * 1e3 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, n, dt = cpu_reference_rate(d, chi, scheme, explicit, budget_s=args.cpu_budget)
+        rate, n, dt = cpu_reference_rate(cfg, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                                 "sample": f"{n} Trotter steps ({dt:.1f} s) of the NumPy/LAPACK oracle on the same "
                                           f"config, OpenBLAS threads = {os.cpu_count()}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if graph_path:
+        dev.close()
     ctx.close()
     if ws > 1:
         import torch.distributed as dist

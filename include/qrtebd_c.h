@@ -163,6 +163,24 @@ qt_status qt_tebd_step_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* con
                                const qt_policy* policy, qt_tensor** sites_out, qt_tensor** bonds_out,
                                qt_bond_report* reports, uint64_t* n_reports);
 
+/* ---- device-resident uniform state (fast path) ----------------------------- */
+/* A UniformMPS kept in HBM across steps (double-buffered site tensors and bond
+ * matrices).  qt_uniform_step performs tebd_step (gates.cpp:513-540) in place;
+ * with use_graph != 0 and stationary bond dimensions (QR scheme, eta == chi)
+ * the step is captured once per buffer-parity pattern and replayed as a
+ * single CUDA graph launch.  Views returned by qt_uniform_view alias the live
+ * buffers (non-owning; invalid after the next step, free the handle with
+ * qt_tensor_free). */
+typedef struct qt_uniform qt_uniform;
+qt_status qt_uniform_create(qt_ctx* ctx, uint64_t cell_length, qt_tensor* const* sites, qt_tensor* const* bonds,
+                            qt_uniform** out);
+qt_status qt_uniform_destroy(qt_uniform* u);
+qt_status qt_uniform_step(qt_uniform* u, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
+                          qt_scheme scheme, const qt_policy* policy, int32_t use_graph, qt_bond_report* reports,
+                          uint64_t* n_reports);
+/* which: 0 = site tensor m, 1 = bond matrix m (bond left of site m) */
+qt_status qt_uniform_view(qt_uniform* u, int which, uint64_t m, qt_tensor** out);
+
 /* ---- observables (proj/src/mps.cpp) --------------------------------------- */
 /* expectation_local(UniformMPS), mps.cpp:168-186: <op> on a site given the
  * bond matrix to its left and the site tensor; out = (re, im). */
@@ -185,8 +203,11 @@ qt_status qt_bond_energy(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m,
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Per-launch CUDA-event profile of the DMMA GEMM kernel (roofline evidence):
  * between begin and end every GEMM launch is bracketed by events; end
- * synchronizes and returns summed algorithmic flops, device ms and launches. */
-qt_status qt_profile_begin(qt_ctx* ctx);
+ * synchronizes and returns summed algorithmic flops, device ms and launches.
+ * Only launches of at least min_flops algorithmic flops are bracketed (each
+ * event pair is a node of the captured step graph; the small Householder
+ * block-reflector products are left out to keep the graph lean). */
+qt_status qt_profile_begin(qt_ctx* ctx, double min_flops);
 qt_status qt_profile_end(qt_ctx* ctx, double* gemm_flops, double* gemm_ms, uint64_t* gemm_launches);
 /* measured FP64 peak of this device in TFLOP/s: kind 0 = DMMA, 1 = DFMA */
 qt_status qt_fp64_peak(qt_ctx* ctx, int kind, double* tflops);

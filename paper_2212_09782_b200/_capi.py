@@ -89,13 +89,18 @@ SIGNATURES = {
     "qt_truncation_error_explicit": (C.c_int, [P, P, P, P, P, DP]),
     "qt_tebd_step_uniform": (C.c_int, [P, C.c_uint64, PP, PP, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int,
                                        C.POINTER(qt_policy), PP, PP, C.POINTER(qt_bond_report), U64P]),
+    "qt_uniform_create": (C.c_int, [P, C.c_uint64, PP, PP, PP]),
+    "qt_uniform_destroy": (C.c_int, [P]),
+    "qt_uniform_step": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int, C.POINTER(qt_policy), C.c_int32,
+                                  C.POINTER(qt_bond_report), U64P]),
+    "qt_uniform_view": (C.c_int, [P, C.c_int, C.c_uint64, PP]),
     "qt_expectation_local": (C.c_int, [P, P, P, P, DP]),
     "qt_schmidt_values": (C.c_int, [P, P, DP, U64P]),
     "qt_right_defect": (C.c_int, [P, P, DP]),
     "qt_eigh": (C.c_int, [P, P, DP, PP]),
     "qt_bond_energy": (C.c_int, [P, P, P, P, P, DP]),
     "qt_fp64_peak": (C.c_int, [P, C.c_int, DP]),
-    "qt_profile_begin": (C.c_int, [P]),
+    "qt_profile_begin": (C.c_int, [P, C.c_double]),
     "qt_profile_end": (C.c_int, [P, DP, DP, U64P]),
 }
 

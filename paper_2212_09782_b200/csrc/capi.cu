@@ -667,6 +667,97 @@ qt_status qt_tebd_step_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* con
   return st;
 }
 
+// ---------------------------------------------------------------- device-resident uniform state
+struct qt_uniform {
+  qt_ctx* ctx = nullptr;
+  qt::UniformDev* dev = nullptr;
+};
+
+qt_status qt_uniform_create(qt_ctx* ctx, uint64_t cell_length, qt_tensor* const* sites, qt_tensor* const* bonds,
+                            qt_uniform** out) {
+  return guard([&] {
+    require(ctx && sites && bonds && out, qt::Err::input, "qt_uniform_create: null argument");
+    const uint64_t L = cell_length;
+    if (L == 0 || L % 2 != 0) throw qt::Error(qt::Err::input, "uniform TEBD needs an even unit cell");
+    std::vector<long long> chi(L);
+    std::vector<const double2*> sp(L), bp(L);
+    const uint64_t d = sites[0] ? sites[0]->shape[0] : 0;
+    for (uint64_t m = 0; m < L; ++m) {
+      require_tensor(sites[m], 3, "uniform site");
+      require_tensor(bonds[m], 2, "uniform bond");
+      if (bonds[m]->shape[0] != bonds[m]->shape[1]) throw qt::Error(qt::Err::shape, "bond matrices must be square");
+      chi[m] = static_cast<long long>(bonds[m]->shape[0]);
+      sp[m] = sites[m]->data;
+      bp[m] = bonds[m]->data;
+    }
+    for (uint64_t m = 0; m < L; ++m)
+      if (sites[m]->shape[0] != d || static_cast<long long>(sites[m]->shape[1]) != chi[m] ||
+          static_cast<long long>(sites[m]->shape[2]) != chi[(m + 1) % L])
+        throw qt::Error(qt::Err::shape, "site tensor shape disagrees with the bond dimensions");
+    auto* u = new qt_uniform;
+    u->ctx = ctx;
+    try {
+      u->dev = qt::uniform_create(ctx->eng, static_cast<int>(L), static_cast<long long>(d), chi, sp, bp);
+    } catch (...) {
+      delete u;
+      throw;
+    }
+    *out = u;
+  });
+}
+
+qt_status qt_uniform_destroy(qt_uniform* u) {
+  return guard([&] {
+    if (!u) return;
+    qt::uniform_destroy(u->dev);
+    delete u;
+  });
+}
+
+qt_status qt_uniform_step(qt_uniform* u, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
+                          qt_scheme scheme, const qt_policy* policy, int32_t use_graph, qt_bond_report* reports,
+                          uint64_t* n_reports) {
+  return guard([&] {
+    require(u && (n_layers == 0 || (parity && gates)), qt::Err::input, "qt_uniform_step: null argument");
+    if (scheme != QT_SCHEME_QR && scheme != QT_SCHEME_QR_CBE)
+      throw qt::Error(qt::Err::input, "scheme not available on the device");
+    const qt_policy pol = policy_or_default(policy);
+    long long shp[3];
+    qt::uniform_live(u->dev, 0, 0, shp);
+    std::vector<std::pair<int, const double2*>> layers;
+    for (uint64_t l = 0; l < n_layers; ++l) {
+      require_gate(gates[l], static_cast<uint64_t>(shp[0]));
+      layers.push_back({parity[l] == 0 ? 0 : 1, gates[l]->data});
+    }
+    const auto recs = qt::uniform_step(u->dev, layers, scheme == QT_SCHEME_QR ? 1 : 0, pol, use_graph != 0);
+    for (const auto& r : recs)
+      if (!r.rep.finite) throw qt::Error(qt::Err::input, "qr_reduced: non-finite entries");
+    const uint64_t cap = n_reports ? *n_reports : 0;
+    for (size_t i = 0; i < recs.size() && i < cap; ++i) {
+      double eps = 0, disc = 0;
+      report_from(recs[i].rep, pol, &eps, &disc);
+      reports[i].bond = static_cast<uint64_t>(recs[i].bond);
+      fill_report(&reports[i].report, recs[i].before, recs[i].eta, recs[i].after, eps, disc, scheme);
+    }
+    if (n_reports) *n_reports = recs.size();
+  });
+}
+
+qt_status qt_uniform_view(qt_uniform* u, int which, uint64_t m, qt_tensor** out) {
+  return guard([&] {
+    require(u && out && (which == 0 || which == 1), qt::Err::input, "qt_uniform_view: bad argument");
+    long long shp[3] = {1, 1, 1};
+    double2* p = qt::uniform_live(u->dev, which, static_cast<int>(m), shp);
+    auto* t = new qt_tensor;
+    t->ctx = u->ctx;
+    t->rank = which == 0 ? 3 : 2;
+    for (int k = 0; k < t->rank; ++k) t->shape[k] = static_cast<uint64_t>(shp[k]);
+    t->data = p;
+    t->owning = false;
+    *out = t;
+  });
+}
+
 // ---------------------------------------------------------------- observables
 qt_status qt_expectation_local(qt_ctx* ctx, const qt_tensor* xi_left, const qt_tensor* b, const qt_tensor* op,
                                double* out2) {
@@ -737,10 +828,10 @@ qt_status qt_bond_energy(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m,
   });
 }
 
-qt_status qt_profile_begin(qt_ctx* ctx) {
+qt_status qt_profile_begin(qt_ctx* ctx, double min_flops) {
   return guard([&] {
     require(ctx != nullptr, qt::Err::input, "null context");
-    qt::gemm_profile_begin();
+    qt::gemm_profile_begin(min_flops);
   });
 }
 

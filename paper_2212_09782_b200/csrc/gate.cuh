@@ -3,6 +3,8 @@
 #pragma once
 
 #include <functional>
+#include <utility>
+#include <vector>
 
 #include "engine.cuh"
 #include "../../include/qrtebd_c.h"
@@ -65,6 +67,20 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
 // singular values of an arbitrary p x q matrix, descending; returns a device
 // pointer (engine slot S_EIG_W) to min(p,q) values
 double* singular_values_device(Engine& e, const double2* m, long long p, long long q);
+
+// device-resident UniformMPS with graph-replayed steps (uniform.cu)
+struct UniformDev;
+UniformDev* uniform_create(Engine& e, int L, long long d, const std::vector<long long>& chi,
+                           const std::vector<const double2*>& sites, const std::vector<const double2*>& bonds);
+void uniform_destroy(UniformDev* s);
+double2* uniform_live(UniformDev* s, int which, int m, long long* shape);
+struct StepRecord {
+  int bond;
+  long long before, eta, after;
+  HostReport rep;
+};
+std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<int, const double2*>>& layers,
+                                     int scheme_qr, const qt_policy& pol, bool use_graph);
 
 // observables (proj/src/mps.cpp)
 void expectation_local(Engine& e, const double2* xi, long long chi_l, const double2* b, long long d,

@@ -30,11 +30,11 @@ namespace {
 // launch profiler: CUDA events around every DMMA GEMM launch (bench roofline)
 struct Prof {
   bool active = false;
-  struct Rec {
-    cudaEvent_t e0, e1;
-    double flops;
-  };
+  double min_flops = 0.0;  // only launches at least this large are bracketed
+  using Rec = GemmProfRec;
   std::vector<Rec> recs;
+  std::vector<Rec> captured;  // recorded while a stream was being captured into a graph
+  GemmProfile replayed;       // accumulated from graph replays
   std::vector<cudaEvent_t> pool;
   size_t next = 0;
   cudaEvent_t event() {
@@ -484,16 +484,32 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
   dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m),
             static_cast<unsigned>(d.batch * splits));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  if (g_prof.active) {
-    ev0 = g_prof.event();
-    ev1 = g_prof.event();
-    QT_CUDA(cudaEventRecord(ev0, st));
+  bool capturing = false;
+  const double gflops = 8.0 * d.M * d.N * d.K * d.batch;
+  const bool prof = g_prof.active && gflops >= g_prof.min_flops;
+  if (prof) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    QT_CUDA(cudaStreamIsCapturing(st, &cs));
+    capturing = cs == cudaStreamCaptureStatusActive;
+    if (capturing) {
+      // events baked into a CUDA graph: fresh ones, owned by that graph
+      QT_CUDA(cudaEventCreate(&ev0));
+      QT_CUDA(cudaEventCreate(&ev1));
+      QT_CUDA(cudaEventRecordWithFlags(ev0, st, cudaEventRecordExternal));
+    } else {
+      ev0 = g_prof.event();
+      ev1 = g_prof.event();
+      QT_CUDA(cudaEventRecord(ev0, st));
+    }
   }
   kern<<<grid, C_::THREADS, C_::SMEM, st>>>(tA, tB, p);
   QT_LAUNCHED();
-  if (g_prof.active) {
-    QT_CUDA(cudaEventRecord(ev1, st));
-    g_prof.recs.push_back({ev0, ev1, 8.0 * d.M * d.N * d.K * d.batch});
+  if (prof) {
+    if (capturing)
+      QT_CUDA(cudaEventRecordWithFlags(ev1, st, cudaEventRecordExternal));
+    else
+      QT_CUDA(cudaEventRecord(ev1, st));
+    (capturing ? g_prof.captured : g_prof.recs).push_back({ev0, ev1, gflops});
   }
   if (MODE == 0 && splits > 1) {
     const long long total = static_cast<long long>(d.batch) * d.M * d.N;
@@ -550,14 +566,37 @@ void zgemm(const GemmDesc& d, const GemmScratch& s, cudaStream_t stream, double*
 
 unsigned long long zgemm_launch_count() { return g_kernel_launches.load(); }
 
-void gemm_profile_begin() {
+void gemm_profile_begin(double min_flops) {
+  g_prof.min_flops = min_flops;
   g_prof.active = true;
   g_prof.recs.clear();
   g_prof.next = 0;
+  g_prof.replayed = GemmProfile();
+}
+
+bool gemm_profile_active() { return g_prof.active; }
+
+std::vector<GemmProfRec> gemm_profile_take_captured() {
+  std::vector<GemmProfRec> out;
+  out.swap(g_prof.captured);
+  return out;
+}
+
+void gemm_profile_add_replay(const std::vector<GemmProfRec>& recs) {
+  if (!g_prof.active) return;
+  for (const auto& rec : recs) {
+    QT_CUDA(cudaEventSynchronize(rec.e1));
+    float ms = 0.f;
+    QT_CUDA(cudaEventElapsedTime(&ms, rec.e0, rec.e1));
+    g_prof.replayed.ms += ms;
+    g_prof.replayed.flops += rec.flops;
+    g_prof.replayed.launches += 1;
+  }
 }
 
 GemmProfile gemm_profile_end() {
-  GemmProfile r;
+  GemmProfile r = g_prof.replayed;
+  g_prof.replayed = GemmProfile();
   g_prof.active = false;
   for (const auto& rec : g_prof.recs) {
     QT_CUDA(cudaEventSynchronize(rec.e1));

@@ -15,6 +15,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace qt {
@@ -62,7 +64,17 @@ struct GemmProfile {
   double flops = 0.0, ms = 0.0;
   unsigned long long launches = 0;
 };
-void gemm_profile_begin();
+void gemm_profile_begin(double min_flops = 0.0);
 GemmProfile gemm_profile_end();
+bool gemm_profile_active();
+// GEMM launches captured into a CUDA graph while profiling is active record
+// their event pairs here; the graph owner takes them after capture and
+// accumulates their elapsed times after every replay.
+struct GemmProfRec {
+  cudaEvent_t e0, e1;
+  double flops;
+};
+std::vector<GemmProfRec> gemm_profile_take_captured();
+void gemm_profile_add_replay(const std::vector<GemmProfRec>& recs);
 
 }  // namespace qt

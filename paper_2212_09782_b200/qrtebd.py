@@ -250,6 +250,60 @@ def tebd_step(state: UniformMPS, schedule, scheme: str, policy=None, ctx: Contex
     return new, out
 
 
+class DeviceUniformMPS:
+    """Device-resident UniformMPS with in-place, graph-replayed steps
+    (qt_uniform_*).  The fast path behind tebd_step for long evolutions."""
+
+    def __init__(self, state: UniformMPS, ctx: Context = None):
+        self.ctx = ctx or default_context()
+        L = state.cell_length()
+        sites = (C.c_void_p * L)(*[t.h for t in state.site_tensors])
+        bonds = (C.c_void_p * L)(*[t.h for t in state.bond_matrices])
+        h = C.c_void_p()
+        check(self.ctx.lib.qt_uniform_create(self.ctx.h, L, sites, bonds, C.byref(h)))
+        self.h = h
+        self.L = L
+        self.phys_dim = state.phys_dim
+
+    def close(self):
+        # a destroyed context already released the device memory and stream
+        if self.h and self.ctx.h:
+            self.ctx.lib.qt_uniform_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, schedule, scheme: str, policy=None, use_graph: bool = True):
+        """tebd_step in place; returns [BondReport]."""
+        gates = [_dev(self.ctx, g) for _, g in schedule]
+        self._gates = gates  # keep device gates alive (graphs capture their addresses)
+        par = (C.c_int32 * max(1, len(schedule)))(*[0 if p == "even" else 1 for p, _ in schedule])
+        gh = (C.c_void_p * max(1, len(gates)))(*[g.h for g in gates])
+        cap = len(schedule) * (self.L // 2 + 1)
+        reps = (qt_bond_report * max(1, cap))()
+        n = C.c_uint64(cap)
+        pol = _policy(policy)
+        check(self.ctx.lib.qt_uniform_step(self.h, len(schedule), par, gh, _capi.SCHEME_IDS[scheme], C.byref(pol),
+                                           1 if use_graph else 0, reps, C.byref(n)))
+        return [BondReport(int(reps[i].bond), TruncationReport.from_c(reps[i].report)) for i in range(n.value)]
+
+    def view(self, which: str, m: int) -> DeviceTensor:
+        """Non-owning view of the live site ('site') or bond ('bond') buffer m."""
+        h = C.c_void_p()
+        check(self.ctx.lib.qt_uniform_view(self.h, 0 if which == "site" else 1, m, C.byref(h)))
+        return DeviceTensor(self.ctx, h)
+
+    def snapshot(self) -> UniformMPS:
+        """Owned copies of the live state as a UniformMPS."""
+        sites = [self.ctx.tensor(self.view("site", m).numpy()) for m in range(self.L)]
+        bonds = [self.ctx.tensor(self.view("bond", m).numpy()) for m in range(self.L)]
+        return UniformMPS(self.phys_dim, sites, bonds)
+
+
 def expectation_local(state: UniformMPS, op, site: int, ctx: Context = None) -> complex:
     """expectation_local(UniformMPS), proj/src/mps.cpp:179-186."""
     ctx = ctx or default_context()

@@ -1,0 +1,62 @@
+"""Device-resident UniformMPS (qt_uniform_*): graph-replayed steps must be
+bitwise identical to eager steps and to the value-semantics tebd_step."""
+import numpy as np
+import pytest
+
+from oracle import qrtebd_oracle as ref
+from paper_2212_09782_b200 import model
+from paper_2212_09782_b200 import qrtebd as q
+
+pytestmark = pytest.mark.gpu
+
+
+def random_state(ctx, d, chi, seed):
+    rng = np.random.default_rng(seed)
+    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(2)]
+    bonds = []
+    for _ in range(2):
+        x = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+        bonds.append(x / np.linalg.norm(x))
+    return q.UniformMPS.from_numpy(ctx, d, sites, bonds)
+
+
+@pytest.mark.parametrize("d,chi", [(3, 16), (5, 40)])
+def test_graph_steps_bitwise_equal_eager_and_tebd_step(ctx, d, chi):
+    sched = model.trotter_schedule(model.bond_hamiltonian(d, 2.0), 0.05, 2)
+    gates = [(p, ctx.tensor(g)) for p, g in sched]
+    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0)
+    st = random_state(ctx, d, chi, 11)
+    ref_state = st
+    dev_g = q.DeviceUniformMPS(st, ctx)
+    dev_e = q.DeviceUniformMPS(st, ctx)
+    for k in range(6):
+        ref_state, rep_v = q.tebd_step(ref_state, gates, "qr", pol, ctx)
+        rep_g = dev_g.step(gates, "qr", pol, use_graph=True)
+        rep_e = dev_e.step(gates, "qr", pol, use_graph=False)
+        assert [r.bond for r in rep_g] == [r.bond for r in rep_v]
+        for a, b in zip(rep_g, rep_v):
+            assert a.report.eps_trunc == b.report.eps_trunc and a.report.chi_after == b.report.chi_after
+        for m in range(2):
+            v = ref_state.site_tensors[m].numpy()
+            assert np.array_equal(dev_g.view("site", m).numpy(), v)
+            assert np.array_equal(dev_e.view("site", m).numpy(), v)
+            assert np.array_equal(dev_g.view("bond", m).numpy(), ref_state.bond_matrices[m].numpy())
+
+
+def test_device_state_grows_bond_dimension_eagerly(ctx):
+    # from a product state the dimensions change every step (no graph), qr_cbe
+    d = 3
+    v = np.zeros(d, dtype=complex)
+    v[0] = 1
+    st = q.product_state_uniform(d, 2, v, ctx)
+    sched = model.trotter_schedule(model.bond_hamiltonian(d, 2.0), 0.05, 2)
+    pol = q.TruncationPolicy(chi_max=32, sv_cutoff=1e-14)
+    dev = q.DeviceUniformMPS(st, ctx)
+    st_o = ref.product_state_uniform(d, 2, v)
+    z = model.clock_operators(d)[0]
+    for _ in range(4):
+        dev.step(sched, "qr_cbe", pol)
+        st_o, _ = ref.tebd_step_uniform(st_o, sched, "qr_cbe", ref.TruncationPolicy(chi_max=32, sv_cutoff=1e-14))
+    snap = dev.snapshot()
+    for s in range(2):
+        assert abs(q.expectation_local(snap, z, s, ctx) - ref.expectation_local(st_o, z, s)) < 1e-10

@@ -17,13 +17,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1)
     a = ap.parse_args()
-    desc, d, chi, scheme, explicit = bench.CONFIGS[a.config]
+    desc, d, chi, scheme, explicit, _ = bench.CONFIGS[a.config]
     ctx = _capi.Context(0)
     sites, bonds = bench.synthetic_state(d, chi)
     st = q.UniformMPS.from_numpy(ctx, d, sites, bonds)
     sched = [(p, ctx.tensor(model.make_gate(model.bond_hamiltonian(d, 2.0), dte)))
              for p, dte in model.layer_structure(0.05, 2)]
-    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=explicit)
+    pol = q.TruncationPolicy(**bench.policy_kw(bench.CONFIGS[a.config]))
     for _ in range(a.warmup):
         st, _ = q.tebd_step(st, sched, scheme, pol, ctx)
     ctx.synchronize()
