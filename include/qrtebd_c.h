@@ -118,6 +118,8 @@ qt_status qt_tensor_download(const qt_tensor* t, double* host);
 /* asynchronous variants (host memory should be pinned) */
 qt_status qt_tensor_upload_async(qt_tensor* t, const double* host);
 qt_status qt_tensor_download_async(const qt_tensor* t, double* host);
+/* device-to-device copy of equal element counts (stream-ordered on dst's context) */
+qt_status qt_tensor_copy(qt_tensor* dst, const qt_tensor* src);
 
 /* ---- linear algebra (proj/src/linalg.cpp:40-64) --------------------------- */
 /* qr_reduced: m (p x q) = Q (p x k) R (k x q), k = min(p,q), R_ii real >= 0 */

@@ -77,6 +77,7 @@ SIGNATURES = {
     "qt_tensor_download": (C.c_int, [P, DP]),
     "qt_tensor_upload_async": (C.c_int, [P, DP]),
     "qt_tensor_download_async": (C.c_int, [P, DP]),
+    "qt_tensor_copy": (C.c_int, [P, P]),
     "qt_qr_reduced": (C.c_int, [P, P, PP, PP]),
     "qt_lq_reduced": (C.c_int, [P, P, PP, PP]),
     "qt_zgemm": (C.c_int, [P, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int,

@@ -129,8 +129,21 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long n0 = static_cast<long long>(blockIdx.x) * BN;
-  const long long m0 = static_cast<long long>(blockIdx.y) * BM;
+  // grouped rasterization: runs of up to 16 M-tiles share each N-tile, so the
+  // CTAs resident at once stream every B tile (and A panel) from HBM once
+  const long long tiles_m_all = ceil_div(p.M, BM), tiles_n_all = ceil_div(p.N, BN);
+  long long m_tile, n_tile;
+  {
+    constexpr long long GROUP_M = 16;
+    const long long t = blockIdx.x;
+    const long long per_group = GROUP_M * tiles_n_all;
+    const long long first_m = (t / per_group) * GROUP_M;
+    const long long group_m = min(tiles_m_all - first_m, GROUP_M);
+    m_tile = first_m + (t % per_group) % group_m;
+    n_tile = (t % per_group) / group_m;
+  }
+  const long long n0 = n_tile * BN;
+  const long long m0 = m_tile * BM;
   const int z = blockIdx.z;
   const int b = z / p.splits, split = z % p.splits;
   const int nkt = static_cast<int>(ceil_div(p.K, BK));
@@ -344,7 +357,7 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
       double tot = 0.0;
       for (int w = 0; w < NCW; ++w) tot += red[w];
       const long long tiles_m = ceil_div(p.M, BM), tiles_n = ceil_div(p.N, BN);
-      p.tile_sums[(static_cast<long long>(z) * tiles_m + blockIdx.y) * tiles_n + blockIdx.x] = tot;
+      p.tile_sums[(static_cast<long long>(z) * tiles_m + m_tile) * tiles_n + n_tile] = tot;
     }
   }
 }
@@ -481,8 +494,7 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
   if (MODE == 1 && static_cast<size_t>(tiles_m * tiles_n * d.batch) > s.tile_sums_elems)
     throw Error(Err::capacity, "zgemm: tile_sums scratch too small");
 
-  dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m),
-            static_cast<unsigned>(d.batch * splits));
+  dim3 grid(static_cast<unsigned>(tiles_n * tiles_m), 1, static_cast<unsigned>(d.batch * splits));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool capturing = false;
   const double gflops = 8.0 * d.M * d.N * d.K * d.batch;
