@@ -224,6 +224,7 @@ __global__ void gauge_r_kernel(const double2* __restrict__ a, long long lda, dou
 }
 
 #include "qr_panel.cuh"
+#include "larfb_cluster.cuh"
 
 int grid_for(long long total) {
   const long long b = ceil_div(total, 256);
@@ -400,7 +401,7 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
                    ph[0] / (nbp - 1), ph[1] / (nbp - 1), ph[2] / (nbp - 1), ph[3] / (nbp - 1));
     }
     const long long ntr = n - j - nbp;
-    if (ntr > 0) {
+    if (ntr > 0 && !larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, ntr, nbp, true)) {
       GemmDesc g;
       // W = V^H A_trail
       g.M = nbp; g.N = ntr; g.K = mp;
@@ -435,6 +436,7 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
     const double2* Vp = V + j * kp + p * NB;
     const double2* Tp = T + p * NB * NB;
     double2* Qs = q + j * ldq + j;
+    if (larfb_cluster(e, Vp, kp, Tp, Qs, ldq, mp, nq, nbp, false)) continue;
     GemmDesc g;
     g.M = nbp; g.N = nq; g.K = mp;
     g.opA = Op::H; g.A = Vp; g.lda = kp;

@@ -25,9 +25,6 @@
 namespace qt {
 namespace {
 
-constexpr int JB = 16;       // block width
-constexpr int JX = 2 * JB;   // subproblem size
-constexpr int JT = 256;      // threads per CTA
 constexpr int MAX_SWEEPS = 30;
 
 __device__ __forceinline__ void jgrid_sync(unsigned* bar, unsigned nblocks) {
@@ -63,6 +60,7 @@ struct JacobiArgs {
   int N, nb;
   double tol;
   int* sweeps_out;
+  const double* fro2;  // ||G||_F^2 (device)
 };
 
 // complex Jacobi rotation for [[a, c], [c*, b]] (a, b real): U = [[cs, sn],
@@ -82,10 +80,13 @@ __device__ __forceinline__ double rel_off(double a, double b, double2 c) {
   return ac == 0.0 ? 0.0 : (sc > 0.0 ? ac / sc : INFINITY);
 }
 
-__device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double tol) {
+// abs_tol = 1e-22 ||G||_F: below it an off-diagonal element cannot move any
+// eigenvalue the truncation or the spectra can resolve (the reference's own
+// eigh is accurate to ~1e-16 ||G||), so those rotations are skipped
+__device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double tol, double abs_tol) {
   Rot r;
   const double ac = hypot(c.x, c.y);
-  r.active = rel_off(a, b, c) > tol && ac > 1e-300;
+  r.active = rel_off(a, b, c) > tol && ac > abs_tol && ac > 1e-300;
   if (!r.active) {
     r.cs = 1.0;
     r.sn = 0.0;
@@ -100,7 +101,11 @@ __device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double to
   return r;
 }
 
-__global__ void __launch_bounds__(JT) jacobi_kernel(JacobiArgs a) {
+template <int JB>
+__global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
+  constexpr int JX = 2 * JB;   // subproblem size
+  constexpr int JT = JB * 16;  // threads: 16 x (JX/2) register blocks of 2 x JX/16
+  constexpr int CB = JX / 16;  // columns per thread in the tile products
   extern __shared__ double2 jdyn[];
   double2(*S)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn);
   double2(*Jm)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn + JX * (JX + 1));
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(JacobiArgs a) {
   const unsigned G = gridDim.x;
   const int npairs = a.nb / 2;
   const int N = a.N;
+  const double abs_tol = 1e-22 * sqrt(*a.fro2);
   int sweep = 0;
 
   for (; sweep < MAX_SWEEPS; ++sweep) {
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(JacobiArgs a) {
             rp[tid] = p0;
             rq[tid] = q0;
             const double2 c = S[p0][q0];
-            const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, c, a.tol);
+            const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, c, a.tol, abs_tol);
             if (rr.active) mx = fmax(mx, rel_off(S[p0][p0].x, S[q0][q0].x, c));
             rots[tid] = rr;
           }
@@ -209,26 +215,54 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(JacobiArgs a) {
           Jm[i][j] = a.Jbuf[static_cast<long long>(yb) * JX * JX + e];
         }
         __syncthreads();
-        // T1 = S Jy
-        for (int e = tid; e < JX * JX; e += JT) {
-          const int i = e / JX, j = e % JX;
-          double2 s = make_double2(0.0, 0.0);
-#pragma unroll 8
-          for (int l = 0; l < JX; ++l) s = cadd(s, cmul(S[i][l], Jm[l][j]));
-          T1[i][j] = s;
+        // T1 = S Jy: each thread a 2 x CB register block (rows i0, i0+1;
+        // columns jb + 16 q, conflict-free for the 16 lanes of a row pair)
+        const int i0 = (tid >> 4) * 2, jb = tid & 15;
+        {
+          double2 acc[2][CB];
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int qq = 0; qq < CB; ++qq) acc[r][qq] = make_double2(0.0, 0.0);
+#pragma unroll 4
+          for (int l = 0; l < JX; ++l) {
+            const double2 a0 = S[i0][l], a1 = S[i0 + 1][l];
+#pragma unroll
+            for (int qq = 0; qq < CB; ++qq) {
+              const double2 bb = Jm[l][jb + 16 * qq];
+              acc[0][qq] = cadd(acc[0][qq], cmul(a0, bb));
+              acc[1][qq] = cadd(acc[1][qq], cmul(a1, bb));
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int qq = 0; qq < CB; ++qq) T1[i0 + r][jb + 16 * qq] = acc[r][qq];
         }
         __syncthreads();
         if (isG) {
           // out = Jx^H T1
           for (int e = tid; e < JX * JX; e += JT) Jm[e / JX][e % JX] = a.Jbuf[static_cast<long long>(xa) * JX * JX + e];
           __syncthreads();
-          for (int e = tid; e < JX * JX; e += JT) {
-            const int i = e / JX, j = e % JX;
-            double2 s = make_double2(0.0, 0.0);
-#pragma unroll 8
-            for (int l = 0; l < JX; ++l) s = cadd(s, cmul(cconj(Jm[l][i]), T1[l][j]));
-            S[i][j] = s;
+          double2 acc[2][CB];
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int qq = 0; qq < CB; ++qq) acc[r][qq] = make_double2(0.0, 0.0);
+#pragma unroll 4
+          for (int l = 0; l < JX; ++l) {
+            const double2 a0 = cconj(Jm[l][i0]), a1 = cconj(Jm[l][i0 + 1]);
+#pragma unroll
+            for (int qq = 0; qq < CB; ++qq) {
+              const double2 bb = T1[l][jb + 16 * qq];
+              acc[0][qq] = cadd(acc[0][qq], cmul(a0, bb));
+              acc[1][qq] = cadd(acc[1][qq], cmul(a1, bb));
+            }
           }
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int qq = 0; qq < CB; ++qq) S[i0 + r][jb + 16 * qq] = acc[r][qq];
           __syncthreads();
         }
         double2(*O)[JX + 1] = isG ? S : T1;
@@ -335,6 +369,9 @@ __global__ void sqrt_clip_kernel(const double* __restrict__ w, int n, double* s)
 
 void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v) {
   if (n <= 0) return;
+  // 16-wide blocks (32x32 subproblems) below n = 512, 32-wide above: the
+  // subproblem sweep is the critical path for small n, the tile updates for large n
+  const int JB = n <= 512 ? 16 : 32, JX = 2 * JB, JT = 16 * JB;
   int nb = static_cast<int>(ceil_div(n, JB));
   if (nb < 2) nb = 2;
   if (nb & 1) ++nb;
@@ -362,11 +399,13 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   a.nb = nb;
   a.tol = 2.220446049250313e-16;  // relative off-diagonal threshold (unit roundoff)
   a.sweeps_out = sweeps;
+  a.fro2 = fro;
   const size_t jsmem = 3 * JX * (JX + 1) * sizeof(double2);
-  static bool jattr = false;
-  if (!jattr) {
-    QT_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(jsmem)));
-    jattr = true;
+  auto kern = JB == 16 ? jacobi_kernel<16> : jacobi_kernel<32>;
+  static bool jattr[2] = {false, false};
+  if (!jattr[JB == 32]) {
+    QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(jsmem)));
+    jattr[JB == 32] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -378,8 +417,27 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  QT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_kernel, a));
+  static const bool dbg = std::getenv("QT_EIGH_DEBUG") != nullptr;
+  cudaEvent_t d0 = nullptr, d1 = nullptr;
+  if (dbg) {
+    QT_CUDA(cudaEventCreate(&d0));
+    QT_CUDA(cudaEventCreate(&d1));
+    QT_CUDA(cudaEventRecord(d0, e.stream));
+  }
+  QT_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   QT_LAUNCHED();
+  if (dbg) {
+    QT_CUDA(cudaEventRecord(d1, e.stream));
+    int sw = 0;
+    QT_CUDA(cudaMemcpyAsync(&sw, sweeps, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
+    QT_CUDA(cudaStreamSynchronize(e.stream));
+    float ms = 0.f;
+    QT_CUDA(cudaEventElapsedTime(&ms, d0, d1));
+    std::fprintf(stderr, "eigh n=%lld N=%d grid=%d sweeps=%d rounds/sweep=%d time=%.3f ms\n", n, N, grid, sw, nb - 1,
+                 ms);
+    cudaEventDestroy(d0);
+    cudaEventDestroy(d1);
+  }
   int P = 1;
   while (P < N) P <<= 1;
   const size_t smem = static_cast<size_t>(P) * (sizeof(double) + sizeof(int));
