@@ -60,6 +60,16 @@ CONFIGS = {
 }
 
 
+CHAIN_CONFIGS = {
+    # finite open chain, Hastings form, sites sharded over the ranks
+    "c5": dict(desc="C5 finite clock chain N=256, d=5, chi=512, qr, even/odd bonds sharded over ranks "
+                    "(NCCL send/recv of boundary tensors), explicit error on",
+               n=256, d=5, chi=512, scheme="qr", explicit=True),
+    "c5small": dict(desc="finite clock chain N=32, d=3, chi=64, qr (smoke-size C5)", n=32, d=3, chi=64, scheme="qr",
+                    explicit=True),
+}
+
+
 def policy_kw(cfg):
     _, d, chi, scheme, explicit, (dabs, drel) = cfg
     return dict(chi_max=chi, delta_chi_abs=dabs, delta_chi_rel=drel, compute_explicit_error=explicit)
@@ -238,18 +248,143 @@ def run_reference(args, cfg):
     return 0
 
 
+def run_chain(args, cc):
+    """C5: finite chain in Hastings form, contiguous even-aligned site blocks
+    per rank; odd layers exchange the straddling boundary tensors with NCCL
+    send/recv (paper_2212_09782_b200/finite.py).  Strong scaling: the chain is
+    fixed, value = Trotter steps/s of the whole chain from the max over ranks."""
+    import torch
+
+    from paper_2212_09782_b200 import _capi, model
+    from paper_2212_09782_b200 import qrtebd as q
+    from paper_2212_09782_b200.finite import ShardedChain, chain_dims, device_backend, partition, random_chain_state
+
+    if args.impl == "reference":
+        return run_chain_reference(args, cc)
+    ws, rank, local = dist_setup()
+    import torch.distributed as dist_mod
+    dist = dist_mod if ws > 1 else None
+    n, d, chi, scheme, explicit = cc["n"], cc["d"], cc["chi"], cc["scheme"], cc["explicit"]
+    torch.cuda.set_device(local)
+    ctx = _capi.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    dmma_peak = ctx.fp64_peak(0)
+    start, end = partition(n, ws)[rank]
+    sites, bonds, keep = random_chain_state(ctx, n, d, chi, start, end)
+    layers = []
+    for parity, dte in model.layer_structure(0.05, 2):
+        layers.append((0 if parity == "even" else 1,
+                       [ctx.tensor(model.make_gate(model.chain_bond_hamiltonian(d, 2.0, m, n), dte))
+                        for m in range(n - 1)]))
+    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=explicit)
+    chain = ShardedChain(sites, bonds, n, rank, ws, device_backend(ctx, scheme, pol), dist)
+    warmup = max(1, min(args.warmup, 2)) if args.steps <= 3 else args.warmup
+    for _ in range(warmup):
+        chain.step(layers, device=f"cuda:{local}")
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(ws)
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    launches0 = ctx.lib.qt_kernel_launches()
+    step_ms = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        chain.step(layers, device=f"cuda:{local}")
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = sampler.stop()
+    launches = ctx.lib.qt_kernel_launches() - launches0
+    tot_ms = max_over_ranks(sum(step_ms), ws)
+    ms_per_step = tot_ms / args.steps
+    chis = chain_dims(n, d, chi)
+    f_step = 0.0
+    for parity, _ in layers:
+        for m in range(parity, n - 1, 2):
+            cm, cn, cr = chis[m], chis[m + 1], chis[m + 2]
+            eta = min(cn, cm * d, d * cr)
+            f_step += flops_per_update(d, cn, eta, eta, explicit)  # uniform-chi estimate per bond
+    upd_per_step = sum(len(range(p, n - 1, 2)) for p, _ in layers)
+    line = {
+        "metric": METRIC, "value": 1e3 / ms_per_step, "unit": "steps/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+        "config": {"workload": cc["desc"], "n_sites": n, "d": d, "chi": chi, "scheme": scheme,
+                   "explicit_error": explicit, "updates_per_step": upd_per_step,
+                   "parallelism": f"sites sharded x{ws} (contiguous even-aligned blocks)",
+                   "l2": "chain state (GBs) far larger than L2"},
+        "updates_per_s": upd_per_step * 1e3 / ms_per_step,
+        "step_ms": [round(x, 3) for x in step_ms],
+        "roofline": {"bound": "tensor", "achieved": f_step / (ms_per_step * 1e-3) / 1e12 * ws, "peak": dmma_peak * ws,
+                     "unit": "TFLOP/s", "frac": f_step / (ms_per_step * 1e-3) / 1e12 / dmma_peak,
+                     "traffic": None, "kernel": "whole step (all kernels), algorithmic flops / device time",
+                     "flops_per_step": f_step},
+        "gpu_launches": int(launches), "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist_mod.destroy_process_group()
+    return 0
+
+
+def run_chain_reference(args, cc):
+    """CPU reference arm for C5: the oracle's bond update timed on the host
+    cores on a bounded sample (the chain's central chi x chi bonds); a step is
+    extrapolated as (updates per step) x (mean central-bond update time), an
+    upper bound since edge bonds are cheaper."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    from oracle import qrtebd_oracle as ref
+    from paper_2212_09782_b200 import model
+    n, d, chi = cc["n"], cc["d"], cc["chi"]
+    rng = np.random.default_rng(0x51AB)
+    bm = ref.random_right_isometry(rng, d, chi, chi)
+    bn = ref.random_right_isometry(rng, d, chi, chi)
+    xi = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+    xi /= np.linalg.norm(xi)
+    u = model.make_gate(model.chain_bond_hamiltonian(d, 2.0, n // 2, n), 0.05)
+    pol = ref.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=cc["explicit"])
+    ref.apply_gate_qr(xi, bm, bn, u, pol)
+    k = max(1, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(k):
+        ref.apply_gate_qr(xi, bm, bn, u, pol)
+    t_upd = (time.perf_counter() - t0) / k
+    upd = (n - 1) + (n // 2) - 0  # 2 even layers of ceil((n-1)/2) + 1 odd layer of floor((n-1)/2)
+    upd = 2 * len(range(0, n - 1, 2)) + len(range(1, n - 1, 2))
+    rate = 1.0 / (upd * t_upd)
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
+            "steps": k, "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+            "config": {"workload": cc["desc"], "n_sites": n, "d": d, "chi": chi},
+            "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{k} central-bond updates (chi={chi}) of the NumPy/LAPACK oracle, step = "
+                                       f"{upd} updates x mean update time (upper bound)"},
+            "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + sorted(CHAIN_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--path", default="graph", choices=["graph", "value"],
                     help="graph: device-resident state, CUDA-graph step; value: C-ABI tebd_step (new handles)")
     args = ap.parse_args()
+    if args.config in CHAIN_CONFIGS:
+        return run_chain(args, CHAIN_CONFIGS[args.config])
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)

@@ -338,7 +338,9 @@ qt_status qt_tensor_download_async(const qt_tensor* t, double* host) {
 qt_status qt_tensor_copy(qt_tensor* dst, const qt_tensor* src) {
   return guard([&] {
     require(dst && src, qt::Err::input, "qt_tensor_copy: null argument");
-    if (dst->numel() != src->numel()) throw qt::Error(qt::Err::shape, "qt_tensor_copy: element counts differ");
+    if (dst->numel() != src->numel())
+      throw qt::Error(qt::Err::shape, "qt_tensor_copy: element counts differ (" + std::to_string(dst->numel()) +
+                                          " vs " + std::to_string(src->numel()) + ")");
     QT_CUDA(cudaMemcpyAsync(dst->data, src->data, src->numel() * sizeof(double2), cudaMemcpyDeviceToDevice,
                             dst->ctx->eng.stream));
   });

@@ -142,6 +142,54 @@ class ShardedChain:
         return self.reports
 
 
+def chain_dims(n_sites: int, d: int, chi_max: int) -> List[int]:
+    """Bond dimensions of a saturated open chain: chi_m = min(d^m, d^(N-m), chi_max),
+    m = 0..N (chi_0 = chi_N = 1), SURVEY.md §8(d) C5."""
+    out = []
+    for m in range(n_sites + 1):
+        a = min(m, n_sites - m)
+        out.append(1 if a == 0 else int(min(chi_max, d ** min(a, 60))))
+    return out
+
+
+def random_chain_state(ctx, n_sites: int, d: int, chi_max: int, start: int, end: int, seed: int = 0x51AB):
+    """Random right-isometric site tensors and normalized bond matrices for
+    sites [start, end), generated on the device (torch RNG seeded per site so
+    every rank builds bit-identical tensors for the sites it owns; right
+    isometries from the device LQ, proj/src/run.cpp:345-349).  Returns
+    (sites, bonds, keepalive) as device tensors."""
+    import torch
+
+    from . import qrtebd as q
+
+    chi = chain_dims(n_sites, d, chi_max)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    keep, sites, bonds = [], [], []
+    for m in range(start, end):
+        cl, cr = chi[m], chi[m + 1]
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed * 1000003 + m)
+        g = torch.randn(cl, d * cr, dtype=torch.complex128, device=dev, generator=gen)
+        torch.cuda.synchronize()  # torch's stream -> the library's stream
+        _, qm = q.lq_reduced(ctx.wrap(g.data_ptr(), (cl, d * cr)), ctx)  # (cl, d*cr), orthonormal rows
+        qt = torch.empty(cl, d * cr, dtype=torch.complex128, device=dev)
+        from . import _capi
+        dst = ctx.wrap(qt.data_ptr(), (cl, d * cr))  # keep the handle alive across the call
+        _capi.check(ctx.lib.qt_tensor_copy(dst.h, qm.h))
+        ctx.synchronize()
+        b = qt.reshape(cl, d, cr).permute(1, 0, 2).contiguous()
+        if m == 0:
+            x = torch.ones(1, 1, dtype=torch.complex128, device=dev)
+        else:
+            x = torch.randn(cl, cl, dtype=torch.complex128, device=dev, generator=gen)
+            x = x / torch.linalg.vector_norm(x)
+        torch.cuda.synchronize()
+        keep += [g, qt, b, x]
+        sites.append(ctx.wrap(b.data_ptr(), tuple(b.shape)))
+        bonds.append(ctx.wrap(x.data_ptr(), tuple(x.shape)))
+    return sites, bonds, keep
+
+
 def numpy_backend(apply_fn) -> Backend:
     """CPU backend over NumPy tensors (tests: apply_fn = oracle apply_gate)."""
     import torch
