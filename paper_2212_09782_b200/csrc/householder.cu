@@ -181,6 +181,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_kernel(PanelArgs a) {
       a.A[gr * a.lda + k] = v;
       a.V[gr * a.ldv + k] =
           gr > k ? v : (gr == k ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0));
+    } else {
+      a.V[gr * a.ldv + k] = make_double2(0.0, 0.0);  // full 32-wide rows (bulk-copied by larfb)
     }
   }
   if (blockIdx.x == 0)
@@ -372,7 +374,7 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   // QT_PANEL_DEBUG=1: per-column phase timings of the cluster panel (stderr)
   static const bool dbg_on = std::getenv("QT_PANEL_DEBUG") != nullptr;
   static long long* dbg_buf = nullptr;
-  if (dbg_on && !dbg_buf) QT_CUDA(cudaMalloc(&dbg_buf, 4 * NB * sizeof(long long)));
+  if (dbg_on && !dbg_buf) QT_CUDA(cudaMalloc(&dbg_buf, 8 * NB * sizeof(long long)));
   base.dbg = dbg_on ? dbg_buf : nullptr;
 
   for (long long p = 0; p < npan; ++p) {
@@ -387,18 +389,20 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
     pa.T = T + p * NB * NB;
     launch_panel(e, pa, mp);
     if (dbg_on) {
-      long long h[4 * NB];
+      long long h[8 * NB];
       QT_CUDA(cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, e.stream));
       QT_CUDA(cudaStreamSynchronize(e.stream));
-      double ph[4] = {0, 0, 0, 0};
+      // phases of CTA 0 / warp 0 per column: CTA reduce, push, DSMEM wait,
+      // cluster combine, zlarfg, ctw/Z, barrier + broadcast, row pass
+      static const char* names[8] = {"cta_red", "push", "wait", "combine", "refl", "ctwZ", "bcast", "rows"};
+      double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int c = 0; c + 1 < nbp; ++c) {
-        ph[0] += h[c * 4 + 1] - h[c * 4 + 0];      // reduce + push
-        ph[1] += h[c * 4 + 2] - h[c * 4 + 1];      // wait for the cluster partials
-        ph[2] += h[c * 4 + 3] - h[c * 4 + 2];      // combine + reflector
-        ph[3] += h[(c + 1) * 4 + 0] - h[c * 4 + 3];  // fused row pass
+        for (int q = 0; q < 7; ++q) ph[q] += h[c * 8 + q + 1] - h[c * 8 + q];
+        ph[7] += h[(c + 1) * 8 + 0] - h[c * 8 + 7];
       }
-      std::fprintf(stderr, "panel m=%lld nbp=%d cycles/col: push %.0f wait %.0f refl %.0f rows %.0f\n", mp, nbp,
-                   ph[0] / (nbp - 1), ph[1] / (nbp - 1), ph[2] / (nbp - 1), ph[3] / (nbp - 1));
+      std::fprintf(stderr, "panel m=%lld nbp=%d cycles/col:", mp, nbp);
+      for (int q = 0; q < 8; ++q) std::fprintf(stderr, " %s %.0f", names[q], ph[q] / (nbp - 1));
+      std::fprintf(stderr, "\n");
     }
     const long long ntr = n - j - nbp;
     if (ntr > 0 && !larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, ntr, nbp, true)) {

@@ -11,13 +11,14 @@
 // round is
 //   A. one CTA per block pair (I,J): load the 32x32 Hermitian subproblem
 //      G[X,X], X = I u J, run one inner cyclic Jacobi sweep in shared memory
-//      (31 rounds x 16 disjoint complex rotations) and store its unitary J_X;
+//      (31 rounds x 16 disjoint complex rotations, each round one fused
+//      two-sided pass over 2x2 blocks) and store its unitary J_X;
 //   B. every 32x32 tile G[X,Y] <- J_X^H G[X,Y] J_Y and every row chunk
 //      V[r,Y] <- V[r,Y] J_Y.
-// Sweeps stop when no rotation in a full sweep met an off-diagonal element
-// above tol = 1e-16 ||G||_F (absolute accuracy of LAPACK's zheevd), at most
-// 30 sweeps.  Every reduction has a fixed order: results are bitwise
-// reproducible run to run.
+// The matrix is scaled by an exact power of two first.  Sweeps stop when no
+// rotation in a full sweep met the criterion of make_rot, at most 30 sweeps.
+// Every reduction has a fixed order: results are bitwise reproducible run to
+// run.
 #include <cstdio>
 
 #include "gate.cuh"
@@ -71,34 +72,83 @@ struct Rot {
   bool active;
 };
 
-// off-diagonal size relative to the diagonal pair (Demmel-Veselic): rotating
-// whenever |c| > eps sqrt(|a b|) keeps the small eigenvalues of graded PSD
-// Gram matrices (the CBE spectrum) accurate to high relative precision
-__device__ __forceinline__ double rel_off(double a, double b, double2 c) {
-  const double ac = hypot(c.x, c.y);
-  const double sc = sqrt(fabs(a) * fabs(b));
-  return ac == 0.0 ? 0.0 : (sc > 0.0 ? ac / sc : INFINITY);
+// 1/x to full precision: hardware approximation + one Newton step (the
+// rotation only needs a few-ulp accurate angle; the latency of IEEE division
+// sits on the inner sweep's critical path)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
-// abs_tol = 1e-22 ||G||_F: below it an off-diagonal element cannot move any
-// eigenvalue the truncation or the spectra can resolve (the reference's own
-// eigh is accurate to ~1e-16 ||G||), so those rotations are skipped
-__device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double tol, double abs_tol) {
+// power-of-two scale bringing ||G||_F into [1, 2): exact, so the eigenvalues
+// are recovered bit-exactly and the squared magnitudes below cannot underflow
+// above the absolute threshold
+__device__ __forceinline__ double jscale(const double* fro2) {
+  const double nrm = sqrt(*fro2);
+  return nrm > 0.0 && isfinite(nrm) ? ldexp(1.0, -ilogb(nrm)) : 1.0;
+}
+
+// Rotation criterion (squared, on the scaled matrix):
+//  * relative (Demmel-Veselic): |c| > eps sqrt(|a b|) keeps the small
+//    eigenvalues of graded PSD Gram matrices (the CBE spectrum) accurate to
+//    high relative precision;
+//  * absolute: |c| > 1e-22 ||G||_F -- below it an off-diagonal element cannot
+//    move any eigenvalue the truncation or the spectra can resolve (the
+//    reference's own eigh is accurate to ~1e-16 ||G||).
+__device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double tol2, double abs_tol2) {
   Rot r;
-  const double ac = hypot(c.x, c.y);
-  r.active = rel_off(a, b, c) > tol && ac > abs_tol && ac > 1e-300;
+  const double ac2 = fma(c.x, c.x, c.y * c.y);
+  r.active = ac2 > tol2 * fabs(a * b) && ac2 > abs_tol2;
   if (!r.active) {
     r.cs = 1.0;
     r.sn = 0.0;
     r.e = make_double2(1.0, 0.0);
     return r;
   }
-  r.e = make_double2(c.x / ac, -c.y / ac);
-  const double theta = (b - a) / (2.0 * ac);
-  const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-  r.cs = 1.0 / sqrt(t * t + 1.0);
+  const double inv_ac = rsqrt(ac2);
+  r.e = make_double2(c.x * inv_ac, -c.y * inv_ac);
+  const double theta = (b - a) * 0.5 * inv_ac;  // |theta| <= ~1e22 on the scaled matrix
+  const double t = copysign(rcp_nr(fabs(theta) + sqrt(fma(theta, theta, 1.0))), theta);
+  r.cs = rsqrt(fma(t, t, 1.0));
   r.sn = t * r.cs;
   return r;
+}
+
+// pair k of inner round ir of the round-robin over JX local indices, p < q
+__device__ __forceinline__ void inner_pair(int k, int ir, int jx, int& p, int& q) {
+  int a = k - 1 + ir, b = jx - 2 - k + ir;  // rr_slot without the modulo
+  if (a >= jx - 1) a -= jx - 1;
+  if (b >= jx - 1) b -= jx - 1;
+  const int x = k == 0 ? 0 : 1 + a, y = 1 + b;  // slot jx-1-k is never 0
+  p = min(x, y);
+  q = max(x, y);
+}
+
+// rows (p,q) of a 2x2 block <- U^H (rows)
+__device__ __forceinline__ void rot_rows(double2& s00, double2& s01, double2& s10, double2& s11, const Rot& r) {
+  const double2 ce = cconj(r.e);
+  const double2 u0 = cmul(ce, s10), u1 = cmul(ce, s11);
+  const double2 t00 = csub(cscale(s00, r.cs), cscale(u0, r.sn));
+  const double2 t01 = csub(cscale(s01, r.cs), cscale(u1, r.sn));
+  s10 = cadd(cscale(s00, r.sn), cscale(u0, r.cs));
+  s11 = cadd(cscale(s01, r.sn), cscale(u1, r.cs));
+  s00 = t00;
+  s01 = t01;
+}
+
+// columns (p,q) of a 2x2 block <- (cols) U
+__device__ __forceinline__ void rot_cols(double2& s00, double2& s01, double2& s10, double2& s11, const Rot& r) {
+  const double2 v0 = cmul(r.e, s01), v1 = cmul(r.e, s11);
+  const double2 t00 = csub(cscale(s00, r.cs), cscale(v0, r.sn));
+  const double2 t10 = csub(cscale(s10, r.cs), cscale(v1, r.sn));
+  s01 = cadd(cscale(s00, r.sn), cscale(v0, r.cs));
+  s11 = cadd(cscale(s10, r.sn), cscale(v1, r.cs));
+  s00 = t00;
+  s10 = t10;
 }
 
 template <int JB>
@@ -110,8 +160,6 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   double2(*S)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn);
   double2(*Jm)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn + JX * (JX + 1));
   double2(*T1)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn + 2 * JX * (JX + 1));
-  __shared__ Rot rots[JX / 2];
-  __shared__ int rp[JX / 2], rq[JX / 2];
   __shared__ double red[JT];
   __shared__ int done_flag;
 
@@ -119,7 +167,9 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   const unsigned G = gridDim.x;
   const int npairs = a.nb / 2;
   const int N = a.N;
-  const double abs_tol = 1e-22 * sqrt(*a.fro2);
+  const double sc = jscale(a.fro2);
+  const double abs_tol = 1e-22 * sqrt(*a.fro2) * sc;
+  const double abs_tol2 = abs_tol * abs_tol, tol2 = a.tol * a.tol;
   int sweep = 0;
 
   for (; sweep < MAX_SWEEPS; ++sweep) {
@@ -137,48 +187,52 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
           Jm[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
         }
         __syncthreads();
+        // inner cyclic sweep: JX-1 rounds of JB disjoint rotations U_k =
+        // [[cs, sn], [-sn e, cs e]] on (p_k, q_k), each round one pass in
+        // which the thread owning the 2x2 block (k,l) computes U_k and U_l
+        // itself from the current S and writes U_k^H S_kl U_l into the other
+        // S buffer (and J_kl U_l in place): one barrier per round
+        double2(*Sc)[JX + 1] = S;
+        double2(*Sn)[JX + 1] = T1;
         for (int ir = 0; ir < JX - 1; ++ir) {
-          if (tid < JX / 2) {
-            int p0 = rr_slot(tid, ir, JX), q0 = rr_slot(JX - 1 - tid, ir, JX);
-            if (p0 > q0) {
-              const int tmp = p0;
-              p0 = q0;
-              q0 = tmp;
+#pragma unroll
+          for (int bi = 0; bi < (JB * JB) / JT; ++bi) {
+            const int b = tid + bi * JT;
+            const int k = b / JB, l = b % JB;
+            int pk, qk, pl, ql;
+            inner_pair(k, ir, JX, pk, qk);
+            inner_pair(l, ir, JX, pl, ql);
+            const Rot rk = make_rot(Sc[pk][pk].x, Sc[qk][qk].x, Sc[pk][qk], tol2, abs_tol2);
+            const Rot rl = k == l ? rk : make_rot(Sc[pl][pl].x, Sc[ql][ql].x, Sc[pl][ql], tol2, abs_tol2);
+            if (k == l && rk.active) mx = 1.0;
+            double2 s00 = Sc[pk][pl], s01 = Sc[pk][ql], s10 = Sc[qk][pl], s11 = Sc[qk][ql];
+            if (rk.active) rot_rows(s00, s01, s10, s11, rk);
+            if (rl.active) {
+              rot_cols(s00, s01, s10, s11, rl);
+              double2 j00 = Jm[pk][pl], j01 = Jm[pk][ql], j10 = Jm[qk][pl], j11 = Jm[qk][ql];
+              rot_cols(j00, j01, j10, j11, rl);
+              Jm[pk][pl] = j00;
+              Jm[pk][ql] = j01;
+              Jm[qk][pl] = j10;
+              Jm[qk][ql] = j11;
             }
-            rp[tid] = p0;
-            rq[tid] = q0;
-            const double2 c = S[p0][q0];
-            const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, c, a.tol, abs_tol);
-            if (rr.active) mx = fmax(mx, rel_off(S[p0][p0].x, S[q0][q0].x, c));
-            rots[tid] = rr;
+            if (k == l) {  // the rotated pivot block is diagonal and real
+              s00.y = 0.0;
+              s11.y = 0.0;
+              if (rk.active) {
+                s01 = make_double2(0.0, 0.0);
+                s10 = make_double2(0.0, 0.0);
+              }
+            }
+            Sn[pk][pl] = s00;
+            Sn[pk][ql] = s01;
+            Sn[qk][pl] = s10;
+            Sn[qk][ql] = s11;
           }
           __syncthreads();
-          // rows: S[p,:] <- cs S[p,:] - sn conj(e) S[q,:];  S[q,:] <- sn S[p,:] + cs conj(e) S[q,:]
-          for (int e = tid; e < (JX / 2) * JX; e += JT) {
-            const int k = e / JX, j = e % JX;
-            const Rot r = rots[k];
-            if (!r.active) continue;
-            const int p0 = rp[k], q0 = rq[k];
-            const double2 sp = S[p0][j], sq = S[q0][j];
-            const double2 ce = cconj(r.e);
-            S[p0][j] = csub(cscale(sp, r.cs), cscale(cmul(ce, sq), r.sn));
-            S[q0][j] = cadd(cscale(sp, r.sn), cscale(cmul(ce, sq), r.cs));
-          }
-          __syncthreads();
-          // columns of S and of J: X[:,p] <- cs X[:,p] - sn e X[:,q];  X[:,q] <- sn X[:,p] + cs e X[:,q]
-          for (int e = tid; e < (JX / 2) * JX * 2; e += JT) {
-            const int which = e / ((JX / 2) * JX);
-            const int ee = e % ((JX / 2) * JX);
-            const int k = ee / JX, i = ee % JX;
-            const Rot r = rots[k];
-            if (!r.active) continue;
-            const int p0 = rp[k], q0 = rq[k];
-            double2(*X)[JX + 1] = which == 0 ? S : Jm;
-            const double2 xp = X[i][p0], xq = X[i][q0];
-            X[i][p0] = csub(cscale(xp, r.cs), cscale(cmul(r.e, xq), r.sn));
-            X[i][q0] = cadd(cscale(xp, r.sn), cscale(cmul(r.e, xq), r.cs));
-          }
-          __syncthreads();
+          double2(*tmp)[JX + 1] = Sc;
+          Sc = Sn;
+          Sn = tmp;
         }
         for (int e = tid; e < JX * JX; e += JT) a.Jbuf[static_cast<long long>(p) * JX * JX + e] = Jm[e / JX][e % JX];
         __syncthreads();
@@ -285,10 +339,10 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     }
     if (tid == 0) a.cta_max[(sweep & 1) * G + blockIdx.x] = red[0];
     jgrid_sync(a.bar, G);
-    if (tid == 0) {
+    if (tid == 0) {  // converged: no rotation met the criterion in a whole sweep
       double m = 0.0;
       for (unsigned b = 0; b < G; ++b) m = fmax(m, __ldcg(&a.cta_max[(sweep & 1) * G + b]));
-      done_flag = m <= a.tol;
+      done_flag = m == 0.0;
     }
     __syncthreads();
     if (done_flag) break;
@@ -299,7 +353,8 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
 // pad: G_pad = [[G, 0], [0, diag(-(|G|+1) - i)]], V = I
 __global__ void jacobi_setup_kernel(const double2* __restrict__ h, int n, int N, const double* fro, double2* G,
                                     double2* V) {
-  const double shift = -(sqrt(*fro) + 1.0);
+  const double sc = jscale(fro);
+  const double shift = -(sqrt(*fro) * sc + 1.0);
   const long long total = static_cast<long long>(N) * N;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -308,7 +363,7 @@ __global__ void jacobi_setup_kernel(const double2* __restrict__ h, int n, int N,
     if (i < n && j < n) {
       // symmetrize (proj/src/linalg.cpp:87): 0.5 (h + h^H)
       const double2 x = h[static_cast<long long>(i) * n + j], y = h[static_cast<long long>(j) * n + i];
-      g = make_double2(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+      g = make_double2((0.5 * sc) * (x.x + y.x), (0.5 * sc) * (x.y - y.y));
       if (i == j) g.y = 0.0;
     } else if (i == j) {
       g = make_double2(shift - i, 0.0);
@@ -321,7 +376,7 @@ __global__ void jacobi_setup_kernel(const double2* __restrict__ h, int n, int N,
 // sort the N diagonal entries descending (ties: lower index first), write the
 // first n eigenvalues and the matching eigenvector columns (n x n, ld n)
 __global__ void jacobi_sort_kernel(const double2* __restrict__ G, const double2* __restrict__ V, int n, int N,
-                                   double* w, double2* vout) {
+                                   const double* fro, double* w, double2* vout) {
   extern __shared__ unsigned char jsm[];
   int P = 1;
   while (P < N) P <<= 1;
@@ -353,7 +408,8 @@ __global__ void jacobi_sort_kernel(const double2* __restrict__ G, const double2*
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = k2[i];
+  const double inv_sc = 1.0 / jscale(fro);  // exact (power of two)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = k2[i] * inv_sc;
   for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += blockDim.x) {
     const int r = static_cast<int>(e / n), c = static_cast<int>(e % n);
     vout[e] = V[static_cast<long long>(r) * N + idx[c]];
@@ -448,7 +504,7 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
                                  static_cast<int>(smem)));
     attr = smem;
   }
-  jacobi_sort_kernel<<<1, 1024, smem, e.stream>>>(G, V, static_cast<int>(n), N, w, v);
+  jacobi_sort_kernel<<<1, 1024, smem, e.stream>>>(G, V, static_cast<int>(n), N, fro, w, v);
   QT_LAUNCHED();
 }
 

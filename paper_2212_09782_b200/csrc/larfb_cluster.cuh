@@ -15,98 +15,165 @@
 constexpr int LB_THREADS = 256;
 constexpr int LB_MAX_RPC = 128;
 
+// global -> own shared memory bulk copy completing on a local mbarrier
+__device__ __forceinline__ void lb_bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+      "l"(gmem), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+// One cluster per CW-column block of A (CW = 32, 16 or 8: narrow blocks put
+// more SMs on short updates); the cluster's CTAs split the rows (rpc each).
+// Thread t owns column j = t % CW and W rows ib + RS q (RS = 256 / CW).
+template <int CW>
 __global__ void __launch_bounds__(LB_THREADS, 1)
     larfb_cluster_kernel(const double2* __restrict__ V, long long ldv, const double2* __restrict__ T, double2* A,
-                         long long lda, int mp, int ncols, int nbp, int rpc, int use_th) {
+                         long long lda, int mp, int ncols, int nbp, int rpc, int use_th, long long* dbg) {
+  constexpr int RS = LB_THREADS / CW;     // 8, 16, 32
+  constexpr int EW = (NB * CW) / LB_THREADS;  // W entries per thread: 4, 2, 1
+  const bool stamp = dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
+  if (stamp) dbg[0] = clock64();
   extern __shared__ __align__(16) double2 lsm[];
-  double2* Vs = lsm;                        // [rpc][32]
-  double2* As = Vs + rpc * NB;              // [rpc][32]
-  double2* Wp = As + rpc * NB;              // [32][32] partial W, later W2
-  double2* Wf = Wp + NB * NB;               // [32][32] reduced W (all-gathered)
-  double2* Tp = Wf + NB * NB;               // [32][32] T'
-  double2* rs = Tp + NB * NB;               // [CS][rows_owned][32] reduce-scatter inbox
-  __shared__ uint64_t bars[2];
+  double2* Vs = lsm;                 // [rpc][32]
+  double2* As = Vs + rpc * NB;       // [rpc][CW]
+  double2* Wp = As + rpc * CW;       // [32][CW] W2 = T' W
+  double2* Wf = Wp + NB * CW;        // [32][CW] reduced W (all-gathered)
+  double2* Tp = Wf + NB * CW;        // [32][32] T'
+  double2* rs = Tp + NB * NB;        // [CS][rows_owned][CW] reduce-scatter inbox
+  __shared__ uint64_t bars[3];       // reduce-scatter, all-gather, staging
 
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, j = tid % CW, ib = tid / CW;
   const unsigned rank = cluster_rank();
   const int CS = static_cast<int>(gridDim.x);
   const int rows_owned = (NB + CS - 1) / CS;  // W rows i with i % CS == rank
   const int my_rows = (NB - static_cast<int>(rank) + CS - 1) / CS;
-  const long long c0 = static_cast<long long>(blockIdx.y) * NB;
-  const int nc = static_cast<int>(min(static_cast<long long>(NB), ncols - c0));
+  const long long c0 = static_cast<long long>(blockIdx.y) * CW;
+  const int nc = static_cast<int>(min(static_cast<long long>(CW), ncols - c0));
   const int r0 = static_cast<int>(rank) * rpc;
   const int nloc = max(0, min(rpc, mp - r0));
 
   if (tid == 0) {
     pmbar_init(&bars[0], 1);
     pmbar_init(&bars[1], 1);
+    pmbar_init(&bars[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    pmbar_arm(&bars[0], static_cast<unsigned>(CS * my_rows * NB * sizeof(double2)));
-    pmbar_arm(&bars[1], static_cast<unsigned>(NB * NB * sizeof(double2)));
+    pmbar_arm(&bars[0], static_cast<unsigned>(CS * my_rows * CW * sizeof(double2)));
+    pmbar_arm(&bars[1], static_cast<unsigned>(NB * CW * sizeof(double2)));
+    pmbar_arm(&bars[2], static_cast<unsigned>(nloc * (NB + nc) * sizeof(double2)));
   }
-  for (int e = tid; e < rpc * NB; e += LB_THREADS) {
-    const int r = e / NB, c = e % NB;
-    const bool ok = r < nloc;
-    Vs[e] = (ok && c < nbp) ? V[static_cast<long long>(r0 + r) * ldv + c] : make_double2(0.0, 0.0);
-    As[e] = (ok && c < nc) ? A[static_cast<long long>(r0 + r) * lda + c0 + c] : make_double2(0.0, 0.0);
+  __syncthreads();
+  // stage V rows (full 32-wide, zero-padded by the panel) and the A row
+  // slices with bulk copies; zero the rows past the panel and the columns
+  // past A's edge
+  for (int r = tid; r < nloc; r += LB_THREADS) {
+    lb_bulk_g2s(&Vs[r * NB], V + static_cast<long long>(r0 + r) * ldv, NB * sizeof(double2), &bars[2]);
+    lb_bulk_g2s(&As[r * CW], A + static_cast<long long>(r0 + r) * lda + c0, nc * sizeof(double2), &bars[2]);
   }
+  for (int e = nloc * NB + tid; e < rpc * NB; e += LB_THREADS) Vs[e] = make_double2(0.0, 0.0);
+  for (int e = tid; e < rpc * CW; e += LB_THREADS)
+    if (e / CW >= nloc || e % CW >= nc) As[e] = make_double2(0.0, 0.0);
   for (int e = tid; e < NB * NB; e += LB_THREADS) {
     const int i = e / NB, k = e % NB;
     Tp[e] = (i < nbp && k < nbp) ? (use_th ? cconj(T[k * NB + i]) : T[i * NB + k]) : make_double2(0.0, 0.0);
   }
+  pmbar_wait(&bars[2], 0);
+  if (stamp) dbg[1] = clock64();
   cluster_sync_all();  // inputs staged, barriers armed everywhere before any push
+  if (stamp) dbg[2] = clock64();
 
-  // partial W[i][j] = sum_r conj(V[r][i]) A[r][j]; thread: column j = lane, rows i = w + 8q
-  double2 acc[4];
+  // partial W[i][j] = sum_r conj(V[r][i]) A[r][j] over the zero-padded rows
+  // (rpc even), two interleaved chains per entry
+  double2 acc[EW];
+  {
+    double2 a2[EW][2];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
-  for (int r = 0; r < nloc; ++r) {
-    const double2 a = As[r * NB + lane];
+    for (int q = 0; q < EW; ++q) a2[q][0] = a2[q][1] = make_double2(0.0, 0.0);
+#pragma unroll 2
+    for (int r = 0; r < rpc; r += 2) {
+      const double2 a0 = As[r * CW + j], a1 = As[(r + 1) * CW + j];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) cfma_conj(acc[q], Vs[r * NB + w + 8 * q], a);
+      for (int q = 0; q < EW; ++q) {
+        cfma_conj(a2[q][0], Vs[r * NB + ib + RS * q], a0);
+        cfma_conj(a2[q][1], Vs[(r + 1) * NB + ib + RS * q], a1);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EW; ++q) acc[q] = cadd(a2[q][0], a2[q][1]);
   }
+  if (stamp) dbg[3] = clock64() + static_cast<long long>(acc[0].x * 0.0);
   // reduce-scatter: row i -> CTA i % CS, slot (source rank, i / CS)
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = w + 8 * q;
+  for (int q = 0; q < EW; ++q) {
+    const int i = ib + RS * q;
     const unsigned owner = static_cast<unsigned>(i % CS);
-    double2* slot = &rs[(static_cast<int>(rank) * rows_owned + i / CS) * NB + lane];
+    double2* slot = &rs[(static_cast<int>(rank) * rows_owned + i / CS) * CW + j];
     st_async_push(cl_map(slot, owner), acc[q], cl_map(&bars[0], owner));
   }
   pmbar_wait(&bars[0], 0);
-  // owned rows: fixed-order sum over sources, then all-gather into every Wf
-  for (int e = tid; e < my_rows * NB; e += LB_THREADS) {
-    const int li = e / NB, j = e % NB;
+  if (stamp) dbg[4] = clock64();
+  // owned rows: fixed-order sum over sources; one (entry, destination) pair
+  // per thread for the all-gather
+  for (int e = tid; e < my_rows * CW * CS; e += LB_THREADS) {
+    const int ent = e / CS, dst = e % CS;
+    const int li = ent / CW, jj = ent % CW;
     const int i = static_cast<int>(rank) + li * CS;
     double2 s = make_double2(0.0, 0.0);
-    for (int src = 0; src < CS; ++src) s = cadd(s, rs[(src * rows_owned + li) * NB + j]);
-    for (int dst = 0; dst < CS; ++dst) st_async_push(cl_map(&Wf[i * NB + j], dst), s, cl_map(&bars[1], dst));
+    for (int src = 0; src < CS; ++src) s = cadd(s, rs[(src * rows_owned + li) * CW + jj]);
+    st_async_push(cl_map(&Wf[i * CW + jj], dst), s, cl_map(&bars[1], dst));
   }
   pmbar_wait(&bars[1], 0);
-  // W2 = T' W  (into Wp)
+  if (stamp) dbg[5] = clock64();
+  // W2 = T' W  (into Wp), two chains per entry
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = w + 8 * q;
-    double2 s = make_double2(0.0, 0.0);
-    for (int k = 0; k < NB; ++k) s = cadd(s, cmul(Tp[i * NB + k], Wf[k * NB + lane]));
-    Wp[i * NB + lane] = s;
+  for (int q = 0; q < EW; ++q) {
+    const int i = ib + RS * q;
+    double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int k = 0; k < NB; k += 2) {
+      s0 = cadd(s0, cmul(Tp[i * NB + k], Wf[k * CW + j]));
+      s1 = cadd(s1, cmul(Tp[i * NB + k + 1], Wf[(k + 1) * CW + j]));
+    }
+    Wp[i * CW + j] = cadd(s0, s1);
   }
   __syncthreads();
-  // A_r -= V_r W2: thread column j = lane, rows r = w + 8 t
+  if (stamp) dbg[6] = clock64();
+  // A_r -= V_r W2: rows r = ib + RS t, column j, two chains per row
   double2 w2[NB];
 #pragma unroll
-  for (int k = 0; k < NB; ++k) w2[k] = Wp[k * NB + lane];
-  for (int r = w; r < nloc; r += LB_THREADS / 32) {
-    double2 s = As[r * NB + lane];
+  for (int k = 0; k < NB; ++k) w2[k] = Wp[k * CW + j];
+#pragma unroll 2
+  for (int r = ib; r < nloc; r += RS) {
+    double2 s0 = As[r * CW + j], s1 = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int k = 0; k < NB; ++k) cfms(s, Vs[r * NB + k], w2[k]);
-    if (lane < nc) A[static_cast<long long>(r0 + r) * lda + c0 + lane] = s;
+    for (int k = 0; k < NB; k += 2) {
+      cfms(s0, Vs[r * NB + k], w2[k]);
+      cfms(s1, Vs[r * NB + k + 1], w2[k + 1]);
+    }
+    if (j < nc) A[static_cast<long long>(r0 + r) * lda + c0 + j] = cadd(s0, s1);
   }
+  if (stamp) dbg[7] = clock64();
   cluster_sync_all();  // no CTA retires while a peer may still push into it
+  if (stamp) dbg[8] = clock64();
 }
 
-constexpr size_t larfb_cluster_smem(int rpc, int cs) {
-  return (size_t(2) * rpc * NB + 3 * NB * NB + size_t(cs) * ((NB + cs - 1) / cs) * NB) * sizeof(double2);
+constexpr size_t larfb_cluster_smem(int rpc, int cs, int cw) {
+  return (size_t(rpc) * (NB + cw) + 2 * NB * cw + NB * NB + size_t(cs) * ((NB + cs - 1) / cs) * cw) * sizeof(double2);
+}
+
+template <int CW>
+void larfb_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv, const double2* T, double2* A,
+                  long long lda, long long mp, long long ncols, int nbp, long long rpc, bool use_th, long long* dbg) {
+  static bool attr = false;
+  if (!attr) {
+    QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<CW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(larfb_cluster_smem(LB_MAX_RPC, 16, 32))));
+    attr = true;
+  }
+  QT_CUDA(cudaLaunchKernelEx(&cfg, larfb_cluster_kernel<CW>, V, ldv, T, A, lda, static_cast<int>(mp),
+                             static_cast<int>(ncols), nbp, static_cast<int>(rpc), use_th ? 1 : 0, dbg));
 }
 
 // A (mp x ncols, ld lda) <- (I - V T' V^H) A for a panel of nbp <= 32
@@ -115,15 +182,15 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
                    long long mp, long long ncols, int nbp, bool use_th) {
   static int max_cs = -1;
   if (max_cs < 0) {
-    QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(larfb_cluster_smem(LB_MAX_RPC, 1))));
+    QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(larfb_cluster_smem(LB_MAX_RPC, 16, 32))));
     max_cs = 0;
     for (int cs : {16, 8}) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs, 1);
       cfg.blockDim = dim3(LB_THREADS);
-      cfg.dynamicSmemBytes = larfb_cluster_smem(LB_MAX_RPC, 1);
+      cfg.dynamicSmemBytes = larfb_cluster_smem(LB_MAX_RPC, cs, 32);
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = cs;
@@ -132,7 +199,7 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
       cfg.attrs = at;
       cfg.numAttrs = 1;
       int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, larfb_cluster_kernel, &cfg) == cudaSuccess && n >= 1) {
+      if (cudaOccupancyMaxActiveClusters(&n, larfb_cluster_kernel<32>, &cfg) == cudaSuccess && n >= 1) {
         max_cs = cs;
         break;
       }
@@ -145,10 +212,19 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
   rpc = ceil_div(rpc, 8) * 8;
   if (rpc > LB_MAX_RPC) return false;
   const long long cs = ceil_div(mp, rpc);
+  // narrowest column block that keeps <= 8 clusters (one per GPC) in flight
+  int cw = 32;
+  if (ceil_div(ncols, 8) <= 8)
+    cw = 8;
+  else if (ceil_div(ncols, 16) <= 8)
+    cw = 16;
+  static const bool dbg_on = std::getenv("QT_LARFB_DEBUG") != nullptr;
+  static long long* dbg = nullptr;
+  if (dbg_on && !dbg) QT_CUDA(cudaMalloc(&dbg, 16 * sizeof(long long)));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(ceil_div(ncols, NB)));
+  cfg.gridDim = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(ceil_div(ncols, cw)));
   cfg.blockDim = dim3(LB_THREADS);
-  cfg.dynamicSmemBytes = larfb_cluster_smem(static_cast<int>(rpc), static_cast<int>(cs));
+  cfg.dynamicSmemBytes = larfb_cluster_smem(static_cast<int>(rpc), static_cast<int>(cs), cw);
   cfg.stream = e.stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -157,8 +233,22 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  QT_CUDA(cudaLaunchKernelEx(&cfg, larfb_cluster_kernel, V, ldv, T, A, lda, static_cast<int>(mp),
-                             static_cast<int>(ncols), nbp, static_cast<int>(rpc), use_th ? 1 : 0));
+  if (cw == 8)
+    larfb_launch<8>(cfg, V, ldv, T, A, lda, mp, ncols, nbp, rpc, use_th, dbg);
+  else if (cw == 16)
+    larfb_launch<16>(cfg, V, ldv, T, A, lda, mp, ncols, nbp, rpc, use_th, dbg);
+  else
+    larfb_launch<32>(cfg, V, ldv, T, A, lda, mp, ncols, nbp, rpc, use_th, dbg);
   QT_LAUNCHED();
+  if (dbg) {  // QT_LARFB_DEBUG=1: phase timings of CTA (0,0) on stderr
+    long long h[9];
+    QT_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, e.stream));
+    QT_CUDA(cudaStreamSynchronize(e.stream));
+    std::fprintf(stderr,
+                 "larfb mp=%lld ncols=%lld cs=%lld rpc=%lld cw=%d cycles: stage %lld csync %lld W %lld rs %lld ag %lld "
+                 "W2 %lld upd %lld exit %lld\n",
+                 mp, ncols, cs, rpc, cw, h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4],
+                 h[6] - h[5], h[7] - h[6], h[8] - h[7]);
+  }
   return true;
 }

@@ -81,6 +81,17 @@ struct Reflector {
   double beta, pad;
 };
 
+// 1/x: hardware approximation + two Newton steps (full precision; the IEEE
+// division's ~114-cycle latency sits on the per-column critical path)
+__device__ __forceinline__ double prcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // zlarfg on (alpha, ||x||^2): beta real, tau = 0 for an exactly-zero column
 __device__ __forceinline__ Reflector make_reflector(double2 alpha, double xnorm2) {
   Reflector r;
@@ -90,18 +101,39 @@ __device__ __forceinline__ Reflector make_reflector(double2 alpha, double xnorm2
     r.beta = alpha.x;
     r.scale = make_double2(0.0, 0.0);
   } else {
-    const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2);
+    const double nrm = sqrt(fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, xnorm2)));
     r.beta = alpha.x >= 0.0 ? -nrm : nrm;
-    // two reciprocals instead of four divisions (FP64 divide ~114 cycles on B200)
-    const double inv_b = 1.0 / r.beta;
-    r.tau = make_double2((r.beta - alpha.x) * inv_b, -alpha.y * inv_b);
     const double2 den = make_double2(alpha.x - r.beta, alpha.y);
-    const double inv_dd = 1.0 / (den.x * den.x + den.y * den.y);
+    // the two reciprocals are independent: their latencies overlap
+    const double inv_b = prcp(r.beta);
+    const double inv_dd = prcp(fma(den.x, den.x, den.y * den.y));
+    r.tau = make_double2((r.beta - alpha.x) * inv_b, -alpha.y * inv_b);
     r.scale = make_double2(den.x * inv_dd, -den.y * inv_dd);
   }
   return r;
 }
 
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// bulk DSMEM push: `bytes` from local shared memory into a peer CTA's shared
+// memory, completing transaction bytes on the peer's mbarrier
+__device__ __forceinline__ void bulk_push(uint32_t remote_dst, const void* src, unsigned bytes, uint32_t remote_bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(remote_dst),
+      "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes), "r"(remote_bar)
+      : "memory");
+}
+
+// Per column c the critical path is: CTA reduction of the partials (warp 0)
+// -> one bulk DSMEM push per peer CTA -> mbarrier wait -> fixed-order combine
+// and zlarfg (warp 0) -> one CTA barrier -> the fused row pass.  The row pass
+// is lean: the active column x (zero on rows <= c) is broadcast from shared
+// memory and every lane applies y_k -= x (scale conj(tau) w_k) with a zero
+// coefficient on lanes k <= c, so rows need no per-row predicates; only the
+// diagonal row (CTA 0, first two register rows) is special.  The reflector
+// vectors stay UNSCALED in registers (v_l = scale_l x^(l)) -- the scale is
+// folded into the T-factor terms at combine time and applied once at the end.
 template <int RPW>
 __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs a) {
   constexpr int RPC = CL_WARPS * RPW;  // rows per CTA
@@ -111,21 +143,22 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
   double2* recv = red + CL_WARPS * NB;       // [2][16][32] partials pushed by every CTA
   double2* rdiag = recv + 2 * 16 * NB;       // [2][32]    diagonal row pushed by CTA 0
   double2* drow = rdiag + 2 * NB;            // [2][32]    diagonal row staged by its owner warp
-  double2* Ts = drow + 2 * NB;               // [32][32]   T factor (CTA 0)
+  double2* mine = drow + 2 * NB;             // [2][32]    this CTA's combined partials (push source)
+  double2* ctws = mine + 2 * NB;             // [32]       conj(tau) w_k of this column
+  double2* Ts = ctws + NB;                   // [32][32]   T factor (CTA 0)
   double2* Z = Ts + NB * NB;                 // [32][32]   z vectors of the T recurrence (CTA 0)
   double2* taus = Z + NB * NB;               // [32]
-  double2* ssum = taus + NB;                 // [32]       combined partials of this column
-  Reflector* refl = reinterpret_cast<Reflector*>(ssum + NB);   // (3 x double2)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ssum + NB + 3);  // [2]
+  Reflector* refl = reinterpret_cast<Reflector*>(taus + NB);   // (3 x double2)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(taus + NB + 3);  // [2]
 
   const int w = threadIdx.x >> 5, k = threadIdx.x & 31;
-  constexpr bool twarp = false;  // T is assembled after the column loop
   const unsigned rank = cluster_rank();
   const int CS = static_cast<int>(gridDim.x);
   const int r0 = static_cast<int>(rank) * RPC;
   const int nloc = max(0, min(RPC, static_cast<int>(a.mp) - r0));
   const int nbp = a.nbp;
-  const unsigned bytes_per_col = static_cast<unsigned>((CS * NB + NB) * sizeof(double2));
+  constexpr unsigned PUSH = NB * sizeof(double2);  // one 32-lane row of double2
+  const unsigned bytes_per_col = static_cast<unsigned>(CS + 1) * PUSH;
 
   if (threadIdx.x == 0) {
     pmbar_init(&bars[0], 1);
@@ -134,35 +167,31 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
     pmbar_arm(&bars[0], bytes_per_col);
     if (nbp > 1) pmbar_arm(&bars[1], bytes_per_col);
   }
+  for (int e = threadIdx.x; e < 2 * 16 * NB; e += CL_THREADS) recv[e] = make_double2(0.0, 0.0);
   double2 y[RPW];
 #pragma unroll
   for (int i = 0; i < RPW; ++i) {
     const int lr = w + CL_WARPS * i;
-    y[i] = (!twarp && lr < nloc && k < nbp) ? a.A[(static_cast<long long>(r0) + lr) * a.lda + k]
-                                             : make_double2(0.0, 0.0);
-    if (!twarp && k == 0) colbuf[lr] = y[i];
-    if (r0 + lr == 0) drow[k] = y[i];
+    const int gr = r0 + lr;
+    y[i] = (lr < nloc && k < nbp) ? a.A[(static_cast<long long>(gr)) * a.lda + k] : make_double2(0.0, 0.0);
+    if (k == 0) colbuf[lr] = gr > 0 ? y[i] : make_double2(0.0, 0.0);
+    if (gr == 0) drow[k] = y[i];
   }
-  if (twarp)
-    for (int e = k; e < NB * NB; e += 32) Ts[e] = make_double2(0.0, 0.0);
+  fence_proxy_async_smem();
   cluster_sync_all();  // barriers initialised and armed everywhere before any push
 
-  // partials for column 0 (rows > 0)
+  // partials for column 0: p_k = sum_{r > 0} conj(x_r) y_rk
   double2 acc = make_double2(0.0, 0.0);
-  if (!twarp) {
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int lr = w + CL_WARPS * i;
-      if (lr < nloc && r0 + lr > 0) cfma_conj(acc, colbuf[lr], y[i]);
-    }
-  }
+  for (int i = 0; i < RPW; ++i) cfma_conj(acc, colbuf[w + CL_WARPS * i], y[i]);
+  double2 my_scale = make_double2(0.0, 0.0);  // scale of the reflector of column k (set at pass k)
 
   for (int c = 0; c < nbp; ++c) {
     const int par = c & 1;
-    const double2* xcol = colbuf + par * RPC;     // column c of every local row
+    const double2* xcol = colbuf + par * RPC;     // column c of every local row (zero on rows <= c)
     double2* ncol = colbuf + (par ^ 1) * RPC;     // column c+1 after this pass
-    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[c * 4 + 0] = clock64();
-    if (!twarp) red[w * NB + k] = acc;
+    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[c * 8 + 0] = clock64();
+    red[w * NB + k] = acc;
     __syncthreads();
     if (w == 0) {
       // four independent chains, then a fixed-order combine
@@ -174,90 +203,108 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
         s2 = cadd(s2, red[(ww + 2) * NB + k]);
         s3 = cadd(s3, red[(ww + 3) * NB + k]);
       }
-      const double2 s = cadd(cadd(s0, s1), cadd(s2, s3));
-      double2* slot = &recv[(par * 16 + rank) * NB + k];
-      for (int r = 0; r < CS; ++r) st_async_push(cl_map(slot, r), s, cl_map(&bars[par], r));
+      mine[par * NB + k] = cadd(cadd(s0, s1), cadd(s2, s3));
+      if (a.dbg && rank == 0 && k == 0) a.dbg[c * 8 + 1] = clock64();
     }
-    if (rank == 0 && w == 1) {
-      // diagonal row c, staged in drow by its owner warp during pass c-1
-      const double2 dv = drow[par * NB + k];
-      for (int r = 0; r < CS; ++r) st_async_push(cl_map(&rdiag[par * NB + k], r), dv, cl_map(&bars[par], r));
+    // warps 0..CS-1 each push this CTA's partials (and, on CTA 0, the diagonal
+    // row) to one peer: the DSMEM stores of the 16 targets issue in parallel
+    if (w < CS) {
+      asm volatile("bar.sync 1, %0;" ::"r"(CS * 32) : "memory");
+      const uint32_t bar_r = cl_map(&bars[par], w);
+      st_async_push(cl_map(&recv[(par * 16 + rank) * NB + k], w), mine[par * NB + k], bar_r);
+      if (rank == 0) st_async_push(cl_map(&rdiag[par * NB + k], w), drow[par * NB + k], bar_r);
     }
-    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[c * 4 + 1] = clock64();
+    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[c * 8 + 2] = clock64();
     if (w == 0) {
       pmbar_wait(&bars[par], (c >> 1) & 1);
       if (k == 0 && c + 2 < nbp) pmbar_arm(&bars[par], bytes_per_col);
-      if (a.dbg && rank == 0 && k == 0) a.dbg[c * 4 + 2] = clock64();
-      double2 sk = make_double2(0.0, 0.0);
-      for (int r = 0; r < CS; ++r) sk = cadd(sk, recv[(par * 16 + r) * NB + k]);
-      ssum[k] = sk;
-      const double sc = __shfl_sync(0xffffffffu, sk.x, c);
-      const Reflector Rw = make_reflector(rdiag[par * NB + c], sc);
+      if (a.dbg && rank == 0 && k == 0) a.dbg[c * 8 + 3] = clock64();
+      // all 16 slots (those of absent CTAs stay zero): loads issue back to
+      // back, then a fixed pairwise tree
+      double2 v[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = recv[(par * 16 + r) * NB + k];
+#pragma unroll
+      for (int h = 8; h >= 2; h >>= 1)
+#pragma unroll
+        for (int r = 0; r < h; ++r) v[r] = cadd(v[r], v[r + h]);
+      const double2 sk = cadd(v[0], v[1]);  // p_k: s_k for k >= c, conj(h_k / conj(scale_k)) for k < c
+      const double2 dk = rdiag[par * NB + k];
+      if (a.dbg && rank == 0 && k == 0) a.dbg[c * 8 + 4] = clock64() + static_cast<long long>(sk.x * 0.0);
+      const Reflector Rw = make_reflector(rdiag[par * NB + c], __shfl_sync(0xffffffffu, sk.x, c));
       if (k == 0) *refl = Rw;
-      // z vector of the T recurrence (zlarft): z_l = -tau (conj(v_c,l) + scale h_l), l < c
+      if (a.dbg && rank == 0 && k == 0) a.dbg[c * 8 + 5] = clock64() + static_cast<long long>(Rw.tau.x * 0.0);
+      // conj(tau) w_k, w_k = a_ck + conj(scale) s_k (zero on lanes that keep their column)
+      ctws[k] = (k > c && k < nbp) ? cmul(cconj(Rw.tau), cadd(dk, cmul(cconj(Rw.scale), sk)))
+                                   : make_double2(0.0, 0.0);
+      // z vector of the T recurrence (zlarft), l < c:
+      //   z_l = -tau (conj(v_c,l) + scale h_l),  v_c,l = scale_l x^(l)_c,  h_l = conj(scale_l) conj(p_l)
       if (rank == 0)
         Z[c * NB + k] = (k < c) ? cmul(make_double2(-Rw.tau.x, -Rw.tau.y),
-                                       cadd(cconj(rdiag[par * NB + k]), cmul(Rw.scale, sk)))
+                                       cadd(cconj(cmul(my_scale, dk)),
+                                            cmul(Rw.scale, cmul(cconj(my_scale), cconj(sk)))))
                                 : make_double2(0.0, 0.0);
+      if (a.dbg && rank == 0 && k == 0) a.dbg[c * 8 + 6] = clock64();
     }
     __syncthreads();
     const Reflector R = *refl;
-    const double2 sk = ssum[k];
-    const double2 a_ck = rdiag[par * NB + k];
-
-    if (rank == 0 && threadIdx.x == 0) taus[c] = R.tau;
-    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[c * 4 + 3] = clock64();
-
-    // fused pass: y_k -= x (scale conj(tau) w_k); v_c = scale x; partials of c+1
-    const double2 ctw = cmul(cconj(R.tau), cadd(a_ck, cmul(cconj(R.scale), sk)));  // conj(tau) w_k
+    const double2 ctw = ctws[k];
     const double2 sctw = cmul(R.scale, ctw);
-    const bool upd = (k > c) && (k < nbp);
+    if (k == c) my_scale = R.scale;
+    if (rank == 0 && threadIdx.x == 0) taus[c] = R.tau;
+    if (a.dbg && rank == 0 && threadIdx.x == 0) a.dbg[c * 8 + 7] = clock64();
+
     const int c1 = c + 1;
+    // rows in chunks whose column-c loads issue back to back (the compiler
+    // cannot hoist a load of xcol above a store to ncol: same array)
+    constexpr int CH = RPW < 6 ? RPW : 5;
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int lr = w + CL_WARPS * i;
-      const int gr = r0 + lr;
-      if (lr < nloc && gr >= c) {  // warp-uniform
-        if (gr == c) {
-          if (upd) y[i] = csub(y[i], ctw);
+    for (int i0 = 0; i0 < RPW; i0 += CH) {
+      double2 xs[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j)
+        if (i0 + j < RPW) xs[j] = xcol[w + CL_WARPS * (i0 + j)];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int i = i0 + j;
+        if (i >= RPW) break;
+        const int lr = w + CL_WARPS * i;
+        const int gr = r0 + lr;
+        cfms(y[i], xs[j], sctw);  // x = 0 on rows <= c: R rows are left alone
+        if (i < 2 && gr == c) {   // the diagonal row (CTA 0 only)
+          y[i] = csub(y[i], ctw);
           if (k == c) y[i] = make_double2(R.beta, 0.0);
-        } else {
-          const double2 x = xcol[lr];
-          if (upd) cfms(y[i], x, sctw);
-          if (k == c) y[i] = cmul(R.scale, x);
         }
-        if (k == c1) ncol[lr] = y[i];
-        if (gr == c1) drow[(par ^ 1) * NB + k] = y[i];  // next diagonal row (CTA 0 only)
+        if (i < 2) {  // rows < 32 exist only on CTA 0: x1 = 0 on rows <= c+1, stage the next diagonal row
+          if (k == c1) ncol[lr] = gr > c1 ? y[i] : make_double2(0.0, 0.0);
+          if (gr == c1) drow[(par ^ 1) * NB + k] = y[i];  // pushed at the top of pass c+1
+        } else if (k == c1) {
+          ncol[lr] = y[i];
+        }
       }
     }
     __syncwarp();
+    // partials of column c+1, two interleaved chains (fixed order)
+    double2 acc1 = make_double2(0.0, 0.0);
     acc = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int lr = w + CL_WARPS * i;
-      // the diagonal row (and rows above c+1) take no part in the next partials
-      if (lr < nloc && r0 + lr > c1) {
-        const double2 x1 = ncol[lr];
-        if (k >= c1)
-          cfma_conj(acc, x1, y[i]);
-        else
-          cfma_conj(acc, y[i], x1);
-      }
-    }
+    for (int i = 0; i < RPW; ++i) cfma_conj((i & 1) ? acc1 : acc, ncol[w + CL_WARPS * i], y[i]);
+    acc = cadd(acc, acc1);
   }
   // all pushes into every CTA have landed (each CTA waited for all columns);
-  // one barrier before retiring so no st.async targets an exited CTA
+  // one barrier before retiring so no bulk copy targets an exited CTA
   cluster_sync_all();
 
-  if (!twarp) {
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int lr = w + CL_WARPS * i;
-      const long long gr = r0 + lr;
-      if (lr < nloc && k < nbp) {
-        a.A[gr * a.lda + k] = y[i];
-        a.V[gr * a.ldv + k] = gr > k ? y[i] : (gr == k ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0));
-      }
+  for (int i = 0; i < RPW; ++i) {
+    const int lr = w + CL_WARPS * i;
+    const long long gr = r0 + lr;
+    if (lr < nloc && k < nbp) {
+      const double2 v = gr > k ? cmul(my_scale, y[i]) : y[i];  // v = scale x^(k) below the diagonal
+      a.A[gr * a.lda + k] = v;
+      a.V[gr * a.ldv + k] = gr > k ? v : (gr == k ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0));
+    } else if (lr < nloc) {
+      a.V[gr * a.ldv + k] = make_double2(0.0, 0.0);  // full 32-wide rows (bulk-copied by larfb)
     }
   }
   if (rank != 0) return;
@@ -285,7 +332,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
 }
 
 constexpr size_t panel_cluster_smem(int rpw) {
-  return (size_t(2 * CL_WARPS * rpw) + CL_WARPS * NB + 2 * 16 * NB + 4 * NB + 2 * NB * NB + 2 * NB + 3) *
+  return (size_t(2 * CL_WARPS * rpw) + CL_WARPS * NB + 2 * 16 * NB + 6 * NB + NB + 2 * NB * NB + NB + 3) *
              sizeof(double2) +
          2 * 8;
 }
