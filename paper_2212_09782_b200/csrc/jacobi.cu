@@ -5,20 +5,23 @@
 // matrix G = L^H L (proj/src/gates.cpp:408-413) and for the Schmidt spectra of
 // the bond matrices (singular values via the Gram matrix).
 //
-// One persistent cooperative kernel per solve.  The matrix is padded to N =
-// 16 * nb (nb even) with decoupled diagonal entries below every eigenvalue.
-// Each sweep runs nb-1 rounds of a round-robin pairing of 16-wide blocks; a
-// round is
-//   A. one CTA per block pair (I,J): load the 32x32 Hermitian subproblem
-//      G[X,X], X = I u J, run one inner cyclic Jacobi sweep in shared memory
-//      (31 rounds x 16 disjoint complex rotations, each round one fused
-//      two-sided pass over 2x2 blocks) and store its unitary J_X;
-//   B. every 32x32 tile G[X,Y] <- J_X^H G[X,Y] J_Y and every row chunk
-//      V[r,Y] <- V[r,Y] J_Y.
-// The matrix is scaled by an exact power of two first.  Sweeps stop when no
-// rotation in a full sweep met the criterion of make_rot, at most 30 sweeps.
-// Every reduction has a fixed order: results are bitwise reproducible run to
-// run.
+// One persistent cooperative kernel per solve.  The matrix is scaled by an
+// exact power of two and padded to N = JB * nb (nb even, JB = 16 for n <= 512,
+// else 32) with decoupled diagonal entries below every eigenvalue.  Each sweep
+// runs nb-1 rounds of a round-robin pairing of JB-wide blocks; a round is
+//   A. one CTA per block pair (I,J): load the 2JB x 2JB Hermitian subproblem
+//      G[X,X], X = I u J, into shared memory and run an inner sweep: JB
+//      "cross" rounds of JB disjoint complex rotations pairing I with J, plus
+//      (first round of a sweep only, when every block meets its pair partner)
+//      JB-1 rounds inside I and J; each inner round forms the rotations once
+//      and applies them two-sidedly in one pass over 2x2 blocks; store J_X;
+//   B. every pair tile G[X,Y] <- J_X^H G[X,Y] J_Y with X <= Y (the tile
+//      (Y,X) is written as its conjugate transpose) and every row chunk
+//      V[r,Y] <- V[r,Y] J_Y, as m8n8k4 DMMA products in shared memory.
+// Rounds are separated by a grid barrier on a monotonic arrival counter.
+// Sweeps stop when no rotation in a full sweep met the criterion of make_rot,
+// at most 30 sweeps.  Every reduction has a fixed order: results are bitwise
+// reproducible run to run.
 #include <cstdio>
 
 #include "gate.cuh"
@@ -28,22 +31,18 @@ namespace {
 
 constexpr int MAX_SWEEPS = 30;
 
-__device__ __forceinline__ void jgrid_sync(unsigned* bar, unsigned nblocks) {
+// grid barrier on a monotonic arrival counter (zeroed by the setup kernel):
+// release-add by every CTA, acquire-poll until epoch * nblocks arrivals
+__device__ __forceinline__ void jgrid_sync(unsigned* bar, unsigned nblocks, unsigned& epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
-    __threadfence();
-    const unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == nblocks - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) {
-      }
-    }
-    __threadfence();
+    ++epoch;
+    const unsigned target = epoch * nblocks;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }
@@ -59,8 +58,10 @@ struct JacobiArgs {
   double* cta_max;  // [gridDim][2]
   unsigned* bar;
   int N, nb;
+  int full_inner;  // 1: full inner sweep in every outer round (QT_JACOBI_FULL)
   double tol;
   int* sweeps_out;
+  long long* prof;  // optional: cycles of CTA 0 in phase A / barrier / phase B / barrier
   const double* fro2;  // ||G||_F^2 (device)
 };
 
@@ -118,14 +119,24 @@ __device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double to
   return r;
 }
 
-// pair k of inner round ir of the round-robin over JX local indices, p < q
-__device__ __forceinline__ void inner_pair(int k, int ir, int jx, int& p, int& q) {
-  int a = k - 1 + ir, b = jx - 2 - k + ir;  // rr_slot without the modulo
-  if (a >= jx - 1) a -= jx - 1;
-  if (b >= jx - 1) b -= jx - 1;
-  const int x = k == 0 ? 0 : 1 + a, y = 1 + b;  // slot jx-1-k is never 0
-  p = min(x, y);
-  q = max(x, y);
+// pair k (< jb) of inner round ir over the 2 jb local indices, p < q:
+// rounds ir < jb pair block I with block J, (k, jb + (k + ir) mod jb); rounds
+// jb <= ir < 2 jb - 1 run a round-robin inside I (k < jb/2) and inside J
+__device__ __forceinline__ void inner_pair(int k, int ir, int jb, int& p, int& q) {
+  if (ir < jb) {
+    int t = k + ir;
+    if (t >= jb) t -= jb;
+    p = k;
+    q = jb + t;
+  } else {
+    const int h = jb / 2, t = ir - jb, kk = k < h ? k : k - h, base = k < h ? 0 : jb;
+    int a = kk - 1 + t, b = jb - 2 - kk + t;  // round-robin slots, modulo jb - 1
+    if (a >= jb - 1) a -= jb - 1;
+    if (b >= jb - 1) b -= jb - 1;
+    const int x = kk == 0 ? 0 : 1 + a, y = 1 + b;
+    p = base + min(x, y);
+    q = base + max(x, y);
+  }
 }
 
 // rows (p,q) of a 2x2 block <- U^H (rows)
@@ -151,12 +162,53 @@ __device__ __forceinline__ void rot_cols(double2& s00, double2& s01, double2& s1
   s10 = t10;
 }
 
+// one m8n8k4 FP64 MMA: c += a b (A row-major 8x4, B column-major 4x8)
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// C = op(A) B for JX x JX complex tiles in shared memory (row stride JX+1),
+// op(A) = A or A^H, on NW warps with DMMA: each warp owns one 8-row block and
+// BPW 8-column blocks; a complex product is four real MMAs
+template <int JX, int NW>
+__device__ __forceinline__ void tile_mm(double2 (*A)[JX + 1], bool conj_t, double2 (*B)[JX + 1],
+                                        double2 (*C)[JX + 1]) {
+  constexpr int NBLK = JX / 8;                  // 8x8 blocks per dimension
+  constexpr int BPW = NBLK * NBLK / NW;         // blocks per warp
+  constexpr int WPR = NBLK / BPW;               // warps per block row
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int rb = w / WPR, cb0 = (w % WPR) * BPW;
+  double cre[BPW][2], cim[BPW][2];
+#pragma unroll
+  for (int b = 0; b < BPW; ++b) cre[b][0] = cre[b][1] = cim[b][0] = cim[b][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < JX; k0 += 4) {
+    const double2 av = conj_t ? cconj(A[k0 + t][rb * 8 + g]) : A[rb * 8 + g][k0 + t];
+#pragma unroll
+    for (int b = 0; b < BPW; ++b) {
+      const double2 bv = B[k0 + t][(cb0 + b) * 8 + g];
+      dmma(cre[b], av.x, bv.x);
+      dmma(cre[b], -av.y, bv.y);
+      dmma(cim[b], av.x, bv.y);
+      dmma(cim[b], av.y, bv.x);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < BPW; ++b) {
+    C[rb * 8 + g][(cb0 + b) * 8 + 2 * t] = make_double2(cre[b][0], cim[b][0]);
+    C[rb * 8 + g][(cb0 + b) * 8 + 2 * t + 1] = make_double2(cre[b][1], cim[b][1]);
+  }
+}
+
 template <int JB>
 __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   constexpr int JX = 2 * JB;   // subproblem size
   constexpr int JT = JB * 16;  // threads: 16 x (JX/2) register blocks of 2 x JX/16
-  constexpr int CB = JX / 16;  // columns per thread in the tile products
   extern __shared__ double2 jdyn[];
+  __shared__ Rot rots[JB];
+  __shared__ int rp[JB], rq[JB];
   double2(*S)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn);
   double2(*Jm)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn + JX * (JX + 1));
   double2(*T1)[JX + 1] = reinterpret_cast<double2(*)[JX + 1]>(jdyn + 2 * JX * (JX + 1));
@@ -171,10 +223,13 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   const double abs_tol = 1e-22 * sqrt(*a.fro2) * sc;
   const double abs_tol2 = abs_tol * abs_tol, tol2 = a.tol * a.tol;
   int sweep = 0;
+  long long pa = 0, pb1 = 0, pbB = 0, pb2 = 0;
+  unsigned epoch = 0;
 
   for (; sweep < MAX_SWEEPS; ++sweep) {
     double mx = 0.0;  // max |offdiag| met by this CTA during the sweep
     for (int round = 0; round < a.nb - 1; ++round) {
+      long long tp0 = (a.prof && tid == 0 && blockIdx.x == 0) ? clock64() : 0;
       // ---------------- phase A: 32x32 subproblems
       for (int p = blockIdx.x; p < npairs; p += G) {
         const int bI = rr_slot(p, round, a.nb), bJ = rr_slot(a.nb - 1 - p, round, a.nb);
@@ -187,25 +242,32 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
           Jm[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
         }
         __syncthreads();
-        // inner cyclic sweep: JX-1 rounds of JB disjoint rotations U_k =
-        // [[cs, sn], [-sn e, cs e]] on (p_k, q_k), each round one pass in
-        // which the thread owning the 2x2 block (k,l) computes U_k and U_l
-        // itself from the current S and writes U_k^H S_kl U_l into the other
-        // S buffer (and J_kl U_l in place): one barrier per round
-        double2(*Sc)[JX + 1] = S;
-        double2(*Sn)[JX + 1] = T1;
-        for (int ir = 0; ir < JX - 1; ++ir) {
-#pragma unroll
-          for (int bi = 0; bi < (JB * JB) / JT; ++bi) {
-            const int b = tid + bi * JT;
+        // inner sweep over the 2JB local indices: JB "cross" rounds pairing
+        // I with J (i, JB + (i + s) mod JB), then JB-1 rounds inside I and J.
+        // The within-block rounds run only in the first outer round of a
+        // sweep (every block is paired there); later rounds of the sweep
+        // rotate the cross pairs only -- every pair is still rotated once per
+        // sweep.  Per inner round: JB threads form the rotations once, then
+        // the thread owning the 2x2 block (k,l) writes U_k^H S_kl U_l and
+        // J_kl U_l in place.
+        const int n_inner = (round == 0 || a.full_inner) ? JX - 1 : JB;
+        for (int ir = 0; ir < n_inner; ++ir) {
+          if (tid < JB) {
+            int p0, q0;
+            inner_pair(tid, ir, JB, p0, q0);
+            const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, S[p0][q0], tol2, abs_tol2);
+            if (rr.active) mx = 1.0;
+            rots[tid] = rr;
+            rp[tid] = p0;
+            rq[tid] = q0;
+          }
+          __syncthreads();
+          for (int b = tid; b < JB * JB; b += JT) {
             const int k = b / JB, l = b % JB;
-            int pk, qk, pl, ql;
-            inner_pair(k, ir, JX, pk, qk);
-            inner_pair(l, ir, JX, pl, ql);
-            const Rot rk = make_rot(Sc[pk][pk].x, Sc[qk][qk].x, Sc[pk][qk], tol2, abs_tol2);
-            const Rot rl = k == l ? rk : make_rot(Sc[pl][pl].x, Sc[ql][ql].x, Sc[pl][ql], tol2, abs_tol2);
-            if (k == l && rk.active) mx = 1.0;
-            double2 s00 = Sc[pk][pl], s01 = Sc[pk][ql], s10 = Sc[qk][pl], s11 = Sc[qk][ql];
+            const Rot rk = rots[k], rl = rots[l];
+            if (!rk.active && !rl.active) continue;
+            const int pk = rp[k], qk = rq[k], pl = rp[l], ql = rq[l];
+            double2 s00 = S[pk][pl], s01 = S[pk][ql], s10 = S[qk][pl], s11 = S[qk][ql];
             if (rk.active) rot_rows(s00, s01, s10, s11, rk);
             if (rl.active) {
               rot_cols(s00, s01, s10, s11, rl);
@@ -224,31 +286,38 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
                 s10 = make_double2(0.0, 0.0);
               }
             }
-            Sn[pk][pl] = s00;
-            Sn[pk][ql] = s01;
-            Sn[qk][pl] = s10;
-            Sn[qk][ql] = s11;
+            S[pk][pl] = s00;
+            S[pk][ql] = s01;
+            S[qk][pl] = s10;
+            S[qk][ql] = s11;
           }
           __syncthreads();
-          double2(*tmp)[JX + 1] = Sc;
-          Sc = Sn;
-          Sn = tmp;
         }
         for (int e = tid; e < JX * JX; e += JT) a.Jbuf[static_cast<long long>(p) * JX * JX + e] = Jm[e / JX][e % JX];
         __syncthreads();
       }
-      jgrid_sync(a.bar, G);
+      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pa += t - tp0; tp0 = t; }
+      jgrid_sync(a.bar, G, epoch);
+      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pb1 += t - tp0; tp0 = t; }
       // ---------------- phase B: tile updates of G and V
+      // G is Hermitian: only pair tiles xa <= yb are computed, the tile
+      // (yb, xa) is written as the conjugate transpose
       const int nrowchunks = N / JX;
-      const int ntiles = npairs * npairs + nrowchunks * npairs;
+      const int ngt = npairs * (npairs + 1) / 2;
+      const int ntiles = ngt + nrowchunks * npairs;
       for (int t = blockIdx.x; t < ntiles; t += G) {
-        const bool isG = t < npairs * npairs;
+        const bool isG = t < ngt;
         int xa, yb, rc = 0;
         if (isG) {
-          xa = t / npairs;
-          yb = t % npairs;
+          int u = t;
+          xa = 0;
+          while (u >= npairs - xa) {
+            u -= npairs - xa;
+            ++xa;
+          }
+          yb = xa + u;
         } else {
-          const int u = t - npairs * npairs;
+          const int u = t - ngt;
           rc = u / npairs;
           yb = u % npairs;
           xa = -1;
@@ -269,54 +338,13 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
           Jm[i][j] = a.Jbuf[static_cast<long long>(yb) * JX * JX + e];
         }
         __syncthreads();
-        // T1 = S Jy: each thread a 2 x CB register block (rows i0, i0+1;
-        // columns jb + 16 q, conflict-free for the 16 lanes of a row pair)
-        const int i0 = (tid >> 4) * 2, jb = tid & 15;
-        {
-          double2 acc[2][CB];
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int qq = 0; qq < CB; ++qq) acc[r][qq] = make_double2(0.0, 0.0);
-#pragma unroll 4
-          for (int l = 0; l < JX; ++l) {
-            const double2 a0 = S[i0][l], a1 = S[i0 + 1][l];
-#pragma unroll
-            for (int qq = 0; qq < CB; ++qq) {
-              const double2 bb = Jm[l][jb + 16 * qq];
-              acc[0][qq] = cadd(acc[0][qq], cmul(a0, bb));
-              acc[1][qq] = cadd(acc[1][qq], cmul(a1, bb));
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int qq = 0; qq < CB; ++qq) T1[i0 + r][jb + 16 * qq] = acc[r][qq];
-        }
+        // T1 = S Jy, then (G tiles) out = Jx^H T1, on the FP64 tensor pipe
+        tile_mm<JX, JT / 32>(S, false, Jm, T1);
         __syncthreads();
         if (isG) {
-          // out = Jx^H T1
           for (int e = tid; e < JX * JX; e += JT) Jm[e / JX][e % JX] = a.Jbuf[static_cast<long long>(xa) * JX * JX + e];
           __syncthreads();
-          double2 acc[2][CB];
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int qq = 0; qq < CB; ++qq) acc[r][qq] = make_double2(0.0, 0.0);
-#pragma unroll 4
-          for (int l = 0; l < JX; ++l) {
-            const double2 a0 = cconj(Jm[l][i0]), a1 = cconj(Jm[l][i0 + 1]);
-#pragma unroll
-            for (int qq = 0; qq < CB; ++qq) {
-              const double2 bb = T1[l][jb + 16 * qq];
-              acc[0][qq] = cadd(acc[0][qq], cmul(a0, bb));
-              acc[1][qq] = cadd(acc[1][qq], cmul(a1, bb));
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int qq = 0; qq < CB; ++qq) S[i0 + r][jb + 16 * qq] = acc[r][qq];
+          tile_mm<JX, JT / 32>(Jm, true, T1, S);
           __syncthreads();
         }
         double2(*O)[JX + 1] = isG ? S : T1;
@@ -326,9 +354,18 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
           const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
           M[static_cast<long long>(gi) * N + gj] = O[i][j];
         }
+        if (isG && xa != yb)
+          for (int e = tid; e < JX * JX; e += JT) {  // mirror, coalesced along i
+            const int j = e / JX, i = e % JX;
+            const int gi = i < JB ? xI * JB + i : xJ * JB + i - JB;
+            const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
+            M[static_cast<long long>(gj) * N + gi] = cconj(O[i][j]);
+          }
         __syncthreads();
       }
-      jgrid_sync(a.bar, G);
+      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pbB += t - tp0; tp0 = t; }
+      jgrid_sync(a.bar, G, epoch);
+      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pb2 += t - tp0; }
     }
     // ---------------- convergence: max over CTAs of the largest rotated element
     red[tid] = mx;
@@ -338,7 +375,7 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
       __syncthreads();
     }
     if (tid == 0) a.cta_max[(sweep & 1) * G + blockIdx.x] = red[0];
-    jgrid_sync(a.bar, G);
+    jgrid_sync(a.bar, G, epoch);
     if (tid == 0) {  // converged: no rotation met the criterion in a whole sweep
       double m = 0.0;
       for (unsigned b = 0; b < G; ++b) m = fmax(m, __ldcg(&a.cta_max[(sweep & 1) * G + b]));
@@ -348,11 +385,18 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     if (done_flag) break;
   }
   if (blockIdx.x == 0 && tid == 0) *a.sweeps_out = sweep + 1;
+  if (a.prof && blockIdx.x == 0 && tid == 0) {
+    a.prof[0] = pa;
+    a.prof[1] = pb1;
+    a.prof[2] = pbB;
+    a.prof[3] = pb2;
+  }
 }
 
 // pad: G_pad = [[G, 0], [0, diag(-(|G|+1) - i)]], V = I
 __global__ void jacobi_setup_kernel(const double2* __restrict__ h, int n, int N, const double* fro, double2* G,
-                                    double2* V) {
+                                    double2* V, unsigned* bar) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) bar[0] = 0;
   const double sc = jscale(fro);
   const double shift = -(sqrt(*fro) * sc + 1.0);
   const long long total = static_cast<long long>(N) * N;
@@ -439,7 +483,7 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   double* fro = e.dscal + SC_TMP2;
   norm2(e, h, n, n, n, fro);
   jacobi_setup_kernel<<<static_cast<int>(std::min<long long>(ceil_div(static_cast<long long>(N) * N, 256), 2048)), 256,
-                        0, e.stream>>>(h, static_cast<int>(n), N, fro, G, V);
+                        0, e.stream>>>(h, static_cast<int>(n), N, fro, G, V, e.barrier + 8);
   QT_LAUNCHED();
   const int grid = std::min(e.num_sms, std::max(npairs, std::min(npairs * npairs + (N / JX) * npairs, e.num_sms)));
   double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8);
@@ -454,7 +498,12 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   a.N = N;
   a.nb = nb;
   a.tol = 2.220446049250313e-16;  // relative off-diagonal threshold (unit roundoff)
+  static const bool full_inner = std::getenv("QT_JACOBI_FULL") != nullptr;
+  a.full_inner = full_inner ? 1 : 0;
   a.sweeps_out = sweeps;
+  static long long* prof = nullptr;
+  if (std::getenv("QT_EIGH_DEBUG") && !prof) QT_CUDA(cudaMalloc(&prof, 8 * sizeof(long long)));
+  a.prof = prof;
   a.fro2 = fro;
   const size_t jsmem = 3 * JX * (JX + 1) * sizeof(double2);
   auto kern = JB == 16 ? jacobi_kernel<16> : jacobi_kernel<32>;
@@ -489,8 +538,13 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
     QT_CUDA(cudaStreamSynchronize(e.stream));
     float ms = 0.f;
     QT_CUDA(cudaEventElapsedTime(&ms, d0, d1));
-    std::fprintf(stderr, "eigh n=%lld N=%d grid=%d sweeps=%d rounds/sweep=%d time=%.3f ms\n", n, N, grid, sw, nb - 1,
-                 ms);
+    long long pc[4] = {0, 0, 0, 0};
+    QT_CUDA(cudaMemcpy(pc, prof, sizeof(pc), cudaMemcpyDeviceToHost));
+    const double rounds = static_cast<double>(sw) * (nb - 1);
+    std::fprintf(stderr,
+                 "eigh n=%lld N=%d grid=%d sweeps=%d rounds/sweep=%d time=%.3f ms | cycles/round: A %.0f sync %.0f B %.0f "
+                 "sync %.0f\n",
+                 n, N, grid, sw, nb - 1, ms, pc[0] / rounds, pc[1] / rounds, pc[2] / rounds, pc[3] / rounds);
     cudaEventDestroy(d0);
     cudaEventDestroy(d1);
   }

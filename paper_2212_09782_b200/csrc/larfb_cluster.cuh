@@ -15,13 +15,10 @@
 constexpr int LB_THREADS = 256;
 constexpr int LB_MAX_RPC = 128;
 
-// global -> own shared memory bulk copy completing on a local mbarrier
-__device__ __forceinline__ void lb_bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-      "l"(gmem), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
-      : "memory");
+__device__ __forceinline__ void lb_cp16(void* smem, const void* gmem, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem), "r"(pred ? 16 : 0)
+               : "memory");
 }
 
 // One cluster per CW-column block of A (CW = 32, 16 or 8: narrow blocks put
@@ -42,7 +39,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   double2* Wf = Wp + NB * CW;        // [32][CW] reduced W (all-gathered)
   double2* Tp = Wf + NB * CW;        // [32][32] T'
   double2* rs = Tp + NB * NB;        // [CS][rows_owned][CW] reduce-scatter inbox
-  __shared__ uint64_t bars[3];       // reduce-scatter, all-gather, staging
+  __shared__ uint64_t bars[2];       // reduce-scatter, all-gather
 
   const int tid = threadIdx.x, j = tid % CW, ib = tid / CW;
   const unsigned rank = cluster_rank();
@@ -57,28 +54,29 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   if (tid == 0) {
     pmbar_init(&bars[0], 1);
     pmbar_init(&bars[1], 1);
-    pmbar_init(&bars[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     pmbar_arm(&bars[0], static_cast<unsigned>(CS * my_rows * CW * sizeof(double2)));
     pmbar_arm(&bars[1], static_cast<unsigned>(NB * CW * sizeof(double2)));
-    pmbar_arm(&bars[2], static_cast<unsigned>(nloc * (NB + nc) * sizeof(double2)));
   }
-  __syncthreads();
   // stage V rows (full 32-wide, zero-padded by the panel) and the A row
-  // slices with bulk copies; zero the rows past the panel and the columns
-  // past A's edge
-  for (int r = tid; r < nloc; r += LB_THREADS) {
-    lb_bulk_g2s(&Vs[r * NB], V + static_cast<long long>(r0 + r) * ldv, NB * sizeof(double2), &bars[2]);
-    lb_bulk_g2s(&As[r * CW], A + static_cast<long long>(r0 + r) * lda + c0, nc * sizeof(double2), &bars[2]);
+  // slices with asynchronous 16-byte copies, all in flight at once; zero-fill
+  // past the panel and past A's edge
+  for (int e = tid; e < rpc * NB; e += LB_THREADS) {
+    const int r = e / NB, c = e % NB;
+    const bool ok = r < nloc;
+    lb_cp16(&Vs[e], ok ? &V[static_cast<long long>(r0 + r) * ldv + c] : V, ok);
   }
-  for (int e = nloc * NB + tid; e < rpc * NB; e += LB_THREADS) Vs[e] = make_double2(0.0, 0.0);
-  for (int e = tid; e < rpc * CW; e += LB_THREADS)
-    if (e / CW >= nloc || e % CW >= nc) As[e] = make_double2(0.0, 0.0);
+  for (int e = tid; e < rpc * CW; e += LB_THREADS) {
+    const int r = e / CW, c = e % CW;
+    const bool ok = r < nloc && c < nc;
+    lb_cp16(&As[e], ok ? &A[static_cast<long long>(r0 + r) * lda + c0 + c] : A, ok);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int e = tid; e < NB * NB; e += LB_THREADS) {
     const int i = e / NB, k = e % NB;
     Tp[e] = (i < nbp && k < nbp) ? (use_th ? cconj(T[k * NB + i]) : T[i * NB + k]) : make_double2(0.0, 0.0);
   }
-  pmbar_wait(&bars[2], 0);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (stamp) dbg[1] = clock64();
   cluster_sync_all();  // inputs staged, barriers armed everywhere before any push
   if (stamp) dbg[2] = clock64();
@@ -113,15 +111,20 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   }
   pmbar_wait(&bars[0], 0);
   if (stamp) dbg[4] = clock64();
-  // owned rows: fixed-order sum over sources; one (entry, destination) pair
-  // per thread for the all-gather
-  for (int e = tid; e < my_rows * CW * CS; e += LB_THREADS) {
-    const int ent = e / CS, dst = e % CS;
-    const int li = ent / CW, jj = ent % CW;
-    const int i = static_cast<int>(rank) + li * CS;
-    double2 s = make_double2(0.0, 0.0);
-    for (int src = 0; src < CS; ++src) s = cadd(s, rs[(src * rows_owned + li) * CW + jj]);
-    st_async_push(cl_map(&Wf[i * CW + jj], dst), s, cl_map(&bars[1], dst));
+  // owned rows: fixed-order sum over sources, then the all-gather; threads
+  // split as (entry, group of destinations)
+  {
+    const int nent = my_rows * CW;
+    const int groups = max(1, min(CS, LB_THREADS / max(1, nent)));
+    for (int e = tid; e < nent * groups; e += LB_THREADS) {
+      const int ent = e / groups, g = e % groups;
+      const int li = ent / CW, jj = ent % CW;
+      const int i = static_cast<int>(rank) + li * CS;
+      double2 s = make_double2(0.0, 0.0);
+      for (int src = 0; src < CS; ++src) s = cadd(s, rs[(src * rows_owned + li) * CW + jj]);
+      for (int dst = g; dst < CS; dst += groups)
+        st_async_push(cl_map(&Wf[i * CW + jj], dst), s, cl_map(&bars[1], dst));
+    }
   }
   pmbar_wait(&bars[1], 0);
   if (stamp) dbg[5] = clock64();
