@@ -58,7 +58,7 @@ class Backend:
 class ShardedChain:
     """The sites [start, end) of an open chain owned by this rank."""
 
-    def __init__(self, sites: Sequence, bonds: Sequence, n_sites: int, rank: int, world: int, backend: Backend,
+    def __init__(self, sites: Sequence, bonds: Sequence, n_sites: int, rank: int, world: int, backend,
                  dist=None):
         self.n = n_sites
         self.rank = rank
@@ -67,7 +67,13 @@ class ShardedChain:
         self.start, self.end = self.blocks[rank]
         self.sites = {m: sites[m - self.start] for m in range(self.start, self.end)}
         self.bonds = {m: bonds[m - self.start] for m in range(self.start, self.end)}
-        self.be = backend
+        # backend: one Backend, or a list whose first entry serves the exchanges
+        # and the straddling bond while the others update interior bonds of a
+        # layer concurrently (one host thread per backend; same-parity bonds
+        # are independent, proj/tests/test_tebd.cc:139-175)
+        pool = list(backend) if isinstance(backend, (list, tuple)) else [backend]
+        self.be = pool[0]
+        self.workers = pool[1:]
         self.dist = dist
         self.reports: List = []
 
@@ -108,8 +114,12 @@ class ShardedChain:
             pending.append((reqs, keep))
         right_hdr = self._post_header(self.rank + 1, device) if has_right_straddle else None
         # interior bonds of this parity (overlap the neighbour's transfer)
-        for m in range(start + parity, end - 1, 2):
-            self._update(m, m + 1, gates[m])
+        interior = list(range(start + parity, end - 1, 2))
+        if self.workers and len(interior) > 1:
+            self._update_concurrent(interior, gates)
+        else:
+            for m in interior:
+                self._update(m, m + 1, gates[m])
         # the straddling bond (end-1, end): owned here, results returned
         if has_right_straddle:
             right_site = self._recv_tensor(self.rank + 1, device, right_hdr)
@@ -133,6 +143,29 @@ class ShardedChain:
         self.bonds[n] = xi
         self.sites[n] = bn
         self.reports.append((n, rep))
+
+    def _update_concurrent(self, bonds_m, gates):
+        """Bond m -> worker m_index % K; each worker runs its bonds in order on
+        its own context (stream + workspace).  Results are committed in bond
+        order, so the chain state and the report list do not depend on the
+        interleaving."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        k = len(self.workers)
+        lanes = [bonds_m[i::k] for i in range(k)]
+
+        def run(i):
+            be = self.workers[i]
+            return [(m, be.apply(self.bonds[m], self.sites[m], self.sites[m + 1], gates[m])) for m in lanes[i]]
+
+        with ThreadPoolExecutor(max_workers=k) as ex:
+            done = dict(kv for part in ex.map(run, range(k)) for kv in part)
+        for m in bonds_m:
+            bm, xi, bn, rep = done[m]
+            self.sites[m] = bm
+            self.bonds[m + 1] = xi
+            self.sites[m + 1] = bn
+            self.reports.append((m + 1, rep))
 
     def step(self, layers: Sequence[Tuple[int, Sequence]], device="cpu"):
         """layers: [(parity 0|1, gates per bond m)] (finite_trotter_layers, gates.hpp:160-173)."""

@@ -108,3 +108,29 @@ def test_partition_is_even_aligned():
             for (s, e), (s2, _) in zip(blocks, blocks[1:]):
                 assert e == s2 and s % 2 == 0 and (e - s) % 2 == 0
             assert len(blocks) <= max(1, n // 2)
+
+
+@pytest.mark.parametrize("workers", [2, 3])
+def test_concurrent_bond_updates_match_sequential(workers):
+    """Same-parity bonds dispatched to several backends (one host thread each,
+    the device path's concurrent streams) give the bitwise result and report
+    order of the sequential chain."""
+    n, d, steps = 9, 2, 3
+    pol = ref.TruncationPolicy(chi_max=6, sv_cutoff=1e-14)
+
+    def apply(xi, bm, bn, u):
+        upd = ref.apply_gate_qr(xi, bm, bn, u, pol)
+        return upd.b_m, upd.xi_n, upd.b_n, upd.report
+
+    layers = layers_for(n, d)
+    runs = []
+    for pool in (numpy_backend(apply), [numpy_backend(apply) for _ in range(workers + 1)]):
+        sites, bonds = make_chain(n, d)
+        chain = ShardedChain(sites, bonds, n, 0, 1, pool)
+        reps = [chain.step(layers) for _ in range(steps)]
+        runs.append((chain, reps))
+    (a, ra), (b, rb) = runs
+    for m in range(n):
+        assert np.array_equal(a.sites[m], b.sites[m])
+        assert np.array_equal(a.bonds[m], b.bonds[m])
+    assert [[m for m, _ in r] for r in ra] == [[m for m, _ in r] for r in rb]
