@@ -538,18 +538,53 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
 
 template <int OPA, int OPB, int MODE>
 void dispatch_shape(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double* r) {
-  // Largest tile that still fills one wave of 148 SMs; the 32x64 tile (two
-  // CTAs per SM) plus automatic split-K covers the small, latency-bound
-  // products of the chi <= 256 updates and the Householder block reflectors.
-  auto tiles = [&](long long bm, long long bn) { return ceil_div(d.M, bm) * ceil_div(d.N, bn) * d.batch; };
-  if (d.M > 32 && tiles(64, 128) >= kNumSMs)
-    launch_cfg<OPA, OPB, 2, 4, 32, 32, 16, 4, MODE>(d, s, st, r);
-  else if (d.M > 32 && tiles(64, 64) >= kNumSMs)
-    launch_cfg<OPA, OPB, 2, 2, 32, 32, 16, 3, MODE>(d, s, st, r);
-  else if (d.M <= 32 && tiles(32, 128) >= kNumSMs)
-    launch_cfg<OPA, OPB, 1, 4, 32, 32, 16, 4, MODE>(d, s, st, r);
-  else
-    launch_cfg<OPA, OPB, 2, 2, 16, 32, 16, 4, MODE>(d, s, st, r);
+  // Tile shape and split-K count from a makespan model: every SM runs
+  // ceil(units / 148) units of bm x bn x (K / splits) complex MACs at the
+  // per-SM FP64 rate (16 CMAC/clk) times a per-tile efficiency, plus the
+  // split-K partial traffic and reduction launch.  Wave quantization is what
+  // matters for the chi <= 512 products (e.g. 1280 x 256 x 1280: 160 tiles of
+  // 32 x 64 = two rounds on 12 SMs; 40 tiles of 64 x 128 split 7 ways = 280
+  // units, 94% balanced on 148 SMs).
+  struct Cand {
+    long long bm, bn;
+    double eff;
+    bool ok;
+  };
+  const Cand cands[4] = {{64, 128, 1.0, d.M > 32}, {64, 64, 0.9, d.M > 32}, {32, 128, 0.95, d.M <= 32},
+                         {32, 64, 0.85, true}};
+  static const bool fixed_split = std::getenv("QT_GEMM_NO_MODEL") != nullptr;
+  const long long nkt = ceil_div(d.K, 16);
+  int best = -1, best_s = 1;
+  double best_t = 1e300;
+  for (int c = 0; c < 4; ++c) {
+    if (!cands[c].ok) continue;
+    const long long tiles = ceil_div(d.M, cands[c].bm) * ceil_div(d.N, cands[c].bn) * d.batch;
+    // split-K only for products whose unsplit tiling is at most two waves
+    // (large products: the partial traffic outweighs the last-wave imbalance)
+    const bool may_split = tiles < 2 * kNumSMs;
+    for (int sp = 1; sp <= 16; ++sp) {
+      if (sp > 1 && (!may_split || MODE == 1 || d.splits > 0 || fixed_split || nkt / sp < 4 ||
+                     static_cast<size_t>(sp) * d.batch * d.M * d.N > s.partial_elems))
+        break;
+      const double rounds = static_cast<double>(ceil_div(tiles * sp, static_cast<long long>(kNumSMs)));
+      const double unit = static_cast<double>(cands[c].bm * cands[c].bn) * 16.0 * ceil_div(nkt, sp);
+      double t = rounds * unit / (31.4e3 * cands[c].eff);  // us
+      if (sp > 1) t += (2.0 * sp + 1.0) * static_cast<double>(d.M * d.N * d.batch) * 16.0 / 6.0e6 + 4.0;
+      if (t < best_t * 0.98) {
+        best_t = t;
+        best = c;
+        best_s = sp;
+      }
+    }
+  }
+  GemmDesc dd = d;
+  if (d.splits <= 0 && !fixed_split) dd.splits = best_s;
+  switch (best) {
+    case 0: launch_cfg<OPA, OPB, 2, 4, 32, 32, 16, 4, MODE>(dd, s, st, r); break;
+    case 1: launch_cfg<OPA, OPB, 2, 2, 32, 32, 16, 3, MODE>(dd, s, st, r); break;
+    case 2: launch_cfg<OPA, OPB, 1, 4, 32, 32, 16, 4, MODE>(dd, s, st, r); break;
+    default: launch_cfg<OPA, OPB, 2, 2, 16, 32, 16, 4, MODE>(dd, s, st, r); break;
+  }
 }
 
 template <int MODE>
