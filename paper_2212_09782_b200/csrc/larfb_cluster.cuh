@@ -21,15 +21,33 @@ __device__ __forceinline__ void lb_cp16(void* smem, const void* gmem, bool pred)
                : "memory");
 }
 
+// XOR swizzle of the 16-byte column slot inside each 8-column group: the
+// m8n8k4 fragment loads (rows r..r+3 x 8 columns, and 8 rows x 4 columns) hit
+// distinct bank groups in every quarter warp
+__device__ __forceinline__ int lb_sw(int row, int col) { return col ^ (((row & 1) << 2) | (row & 2)); }
+
+// one m8n8k4 FP64 MMA: c += a b (A row-major 8x4, B column-major 4x8)
+__device__ __forceinline__ void lb_dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+// complex 8x8x4 block product: (cre + i cim) += a b, four real MMAs
+__device__ __forceinline__ void cmma(double (&cre)[2], double (&cim)[2], double2 a, double2 b) {
+  lb_dmma(cre, a.x, b.x);
+  lb_dmma(cre, -a.y, b.y);
+  lb_dmma(cim, a.x, b.y);
+  lb_dmma(cim, a.y, b.x);
+}
+
 // One cluster per CW-column block of A (CW = 32, 16 or 8: narrow blocks put
 // more SMs on short updates); the cluster's CTAs split the rows (rpc each).
-// Thread t owns column j = t % CW and W rows ib + RS q (RS = 256 / CW).
+// The products run on the FP64 tensor pipe (m8n8k4 DMMA, four real MMAs per
+// complex block) over XOR-swizzled shared-memory tiles.
 template <int CW>
 __global__ void __launch_bounds__(LB_THREADS, 1)
     larfb_cluster_kernel(const double2* __restrict__ V, long long ldv, const double2* __restrict__ T, double2* A,
                          long long lda, int mp, int ncols, int nbp, int rpc, int use_th, long long* dbg) {
-  constexpr int RS = LB_THREADS / CW;     // 8, 16, 32
-  constexpr int EW = (NB * CW) / LB_THREADS;  // W entries per thread: 4, 2, 1
   const bool stamp = dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0;
   if (stamp) dbg[0] = clock64();
   extern __shared__ __align__(16) double2 lsm[];
@@ -41,7 +59,7 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   double2* rs = Tp + NB * NB;        // [CS][rows_owned][CW] reduce-scatter inbox
   __shared__ uint64_t bars[2];       // reduce-scatter, all-gather
 
-  const int tid = threadIdx.x, j = tid % CW, ib = tid / CW;
+  const int tid = threadIdx.x;
   const unsigned rank = cluster_rank();
   const int CS = static_cast<int>(gridDim.x);
   const int rows_owned = (NB + CS - 1) / CS;  // W rows i with i % CS == rank
@@ -64,12 +82,12 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   for (int e = tid; e < rpc * NB; e += LB_THREADS) {
     const int r = e / NB, c = e % NB;
     const bool ok = r < nloc;
-    lb_cp16(&Vs[e], ok ? &V[static_cast<long long>(r0 + r) * ldv + c] : V, ok);
+    lb_cp16(&Vs[r * NB + lb_sw(r, c)], ok ? &V[static_cast<long long>(r0 + r) * ldv + c] : V, ok);
   }
   for (int e = tid; e < rpc * CW; e += LB_THREADS) {
     const int r = e / CW, c = e % CW;
     const bool ok = r < nloc && c < nc;
-    lb_cp16(&As[e], ok ? &A[static_cast<long long>(r0 + r) * lda + c0 + c] : A, ok);
+    lb_cp16(&As[r * CW + lb_sw(r, c)], ok ? &A[static_cast<long long>(r0 + r) * lda + c0 + c] : A, ok);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int e = tid; e < NB * NB; e += LB_THREADS) {
@@ -81,33 +99,59 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   cluster_sync_all();  // inputs staged, barriers armed everywhere before any push
   if (stamp) dbg[2] = clock64();
 
-  // partial W[i][j] = sum_r conj(V[r][i]) A[r][j] over the zero-padded rows
-  // (rpc even), two interleaved chains per entry
-  double2 acc[EW];
+  // partial W = V_r^H A_r (32 x CW) on the FP64 tensor pipe: 8x8 output
+  // blocks, BPW per warp (or KS warps splitting the rows of one block)
+  const int lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  constexpr int CB = CW / 8;                 // column blocks
+  constexpr int OB = 4 * CB;                 // output blocks of W
+  constexpr int BPW = OB >= 8 ? OB / 8 : 1;  // blocks per warp
+  constexpr int KS = OB >= 8 ? 1 : 8 / OB;   // warps per block (row split)
   {
-    double2 a2[EW][2];
+    const int wb = w / KS, kh = w % KS;
+    const int rb = (wb * BPW) / CB;  // BPW divides CB: one block row per warp
+    double cre[BPW][2], cim[BPW][2];
 #pragma unroll
-    for (int q = 0; q < EW; ++q) a2[q][0] = a2[q][1] = make_double2(0.0, 0.0);
+    for (int b = 0; b < BPW; ++b) cre[b][0] = cre[b][1] = cim[b][0] = cim[b][1] = 0.0;
+    const int rlo = kh * (rpc / KS), rhi = rlo + rpc / KS;
 #pragma unroll 2
-    for (int r = 0; r < rpc; r += 2) {
-      const double2 a0 = As[r * CW + j], a1 = As[(r + 1) * CW + j];
+    for (int r = rlo; r < rhi; r += 4) {
+      const int rr = r + t;
+      const double2 av = cconj(Vs[rr * NB + lb_sw(rr, rb * 8 + g)]);
 #pragma unroll
-      for (int q = 0; q < EW; ++q) {
-        cfma_conj(a2[q][0], Vs[r * NB + ib + RS * q], a0);
-        cfma_conj(a2[q][1], Vs[(r + 1) * NB + ib + RS * q], a1);
+      for (int b = 0; b < BPW; ++b) {
+        const int cb = (wb * BPW + b) % CB;
+        const double2 bv = As[rr * CW + lb_sw(rr, cb * 8 + g)];
+        cmma(cre[b], cim[b], av, bv);
       }
     }
+    if (KS > 1) {  // combine the row halves in a fixed order through Wp
+      if (kh == 1)
 #pragma unroll
-    for (int q = 0; q < EW; ++q) acc[q] = cadd(a2[q][0], a2[q][1]);
-  }
-  if (stamp) dbg[3] = clock64() + static_cast<long long>(acc[0].x * 0.0);
-  // reduce-scatter: row i -> CTA i % CS, slot (source rank, i / CS)
+        for (int e2 = 0; e2 < 2; ++e2)
+          Wp[(rb * 8 + g) * CW + (wb % CB) * 8 + 2 * t + e2] = make_double2(cre[0][e2], cim[0][e2]);
+      __syncthreads();
+      if (kh == 0)
 #pragma unroll
-  for (int q = 0; q < EW; ++q) {
-    const int i = ib + RS * q;
-    const unsigned owner = static_cast<unsigned>(i % CS);
-    double2* slot = &rs[(static_cast<int>(rank) * rows_owned + i / CS) * CW + j];
-    st_async_push(cl_map(slot, owner), acc[q], cl_map(&bars[0], owner));
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const double2 o = Wp[(rb * 8 + g) * CW + (wb % CB) * 8 + 2 * t + e2];
+          cre[0][e2] += o.x;
+          cim[0][e2] += o.y;
+        }
+    }
+    if (stamp) dbg[3] = clock64() + static_cast<long long>(cre[0][0] * 0.0);
+    // reduce-scatter: row i -> CTA i % CS, slot (source rank, i / CS)
+    if (kh == 0) {
+      const int i = rb * 8 + g;
+      const unsigned owner = static_cast<unsigned>(i % CS);
+#pragma unroll
+      for (int b = 0; b < BPW; ++b)
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int jj = ((wb * BPW + b) % CB) * 8 + 2 * t + e2;
+          double2* slot = &rs[(static_cast<int>(rank) * rows_owned + i / CS) * CW + jj];
+          st_async_push(cl_map(slot, owner), make_double2(cre[b][e2], cim[b][e2]), cl_map(&bars[0], owner));
+        }
+    }
   }
   pmbar_wait(&bars[0], 0);
   if (stamp) dbg[4] = clock64();
@@ -128,33 +172,50 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   }
   pmbar_wait(&bars[1], 0);
   if (stamp) dbg[5] = clock64();
-  // W2 = T' W  (into Wp), two chains per entry
+  // W2 = T' W (32 x CW, K = 32) into Wp
+  if (w < OB / BPW) {
+    const int rb = (w * BPW) / CB;
+    double cre[BPW][2], cim[BPW][2];
 #pragma unroll
-  for (int q = 0; q < EW; ++q) {
-    const int i = ib + RS * q;
-    double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
-#pragma unroll 8
-    for (int k = 0; k < NB; k += 2) {
-      s0 = cadd(s0, cmul(Tp[i * NB + k], Wf[k * CW + j]));
-      s1 = cadd(s1, cmul(Tp[i * NB + k + 1], Wf[(k + 1) * CW + j]));
+    for (int b = 0; b < BPW; ++b) cre[b][0] = cre[b][1] = cim[b][0] = cim[b][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < NB; k0 += 4) {
+      const double2 av = Tp[(rb * 8 + g) * NB + k0 + t];
+#pragma unroll
+      for (int b = 0; b < BPW; ++b) {
+        const int cb = (w * BPW + b) % CB;
+        cmma(cre[b], cim[b], av, Wf[(k0 + t) * CW + cb * 8 + g]);
+      }
     }
-    Wp[i * CW + j] = cadd(s0, s1);
+#pragma unroll
+    for (int b = 0; b < BPW; ++b)
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2)
+        Wp[(rb * 8 + g) * CW + ((w * BPW + b) % CB) * 8 + 2 * t + e2] = make_double2(cre[b][e2], cim[b][e2]);
   }
   __syncthreads();
   if (stamp) dbg[6] = clock64();
-  // A_r -= V_r W2: rows r = ib + RS t, column j, two chains per row
-  double2 w2[NB];
+  // A_r <- A_r - V_r W2 on the tensor pipe: 8x8 blocks of the rpc x CW slice
+  for (int blk = w; blk < (rpc / 8) * CB; blk += LB_THREADS / 32) {
+    const int rb = blk / CB, cb = blk % CB, row = rb * 8 + g;
+    double cre[2], cim[2];
 #pragma unroll
-  for (int k = 0; k < NB; ++k) w2[k] = Wp[k * CW + j];
-#pragma unroll 2
-  for (int r = ib; r < nloc; r += RS) {
-    double2 s0 = As[r * CW + j], s1 = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int k = 0; k < NB; k += 2) {
-      cfms(s0, Vs[r * NB + k], w2[k]);
-      cfms(s1, Vs[r * NB + k + 1], w2[k + 1]);
+    for (int e2 = 0; e2 < 2; ++e2) {
+      const double2 c = As[row * CW + lb_sw(row, cb * 8 + 2 * t + e2)];
+      cre[e2] = c.x;
+      cim[e2] = c.y;
     }
-    if (j < nc) A[static_cast<long long>(r0 + r) * lda + c0 + j] = cadd(s0, s1);
+#pragma unroll
+    for (int k0 = 0; k0 < NB; k0 += 4) {
+      const double2 av = Vs[row * NB + lb_sw(row, k0 + t)];
+      cmma(cre, cim, make_double2(-av.x, -av.y), Wp[(k0 + t) * CW + cb * 8 + g]);
+    }
+    if (row < nloc)
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int col = cb * 8 + 2 * t + e2;
+        if (col < nc) A[static_cast<long long>(r0 + row) * lda + c0 + col] = make_double2(cre[e2], cim[e2]);
+      }
   }
   if (stamp) dbg[7] = clock64();
   cluster_sync_all();  // no CTA retires while a peer may still push into it
