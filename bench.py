@@ -380,6 +380,31 @@ def run_chain_reference(args, cc):
     return 0
 
 
+def gemm_traffic(config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    GEMM shape of this configuration, from the committed ncu --set full
+    capture summarised in profiles/r01_ncu_full_summary.txt (C2: the
+    1280 x 256 x 1280 projection; north star: 5120 x 1024 x 5120); None when
+    no capture of that shape exists."""
+    row = {"c2": "zgemm_c2.ncu-rep", "north": "zgemm_north.ncu-rep"}.get(config)
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_full_summary.txt")
+    if row is None or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        lines = f.read().splitlines()
+    cols = lines[0].split()
+    for ln in lines[1:]:
+        if ln.startswith(row):
+            vals = ln.split()
+            # report and kernel name are the leading fields; metrics are the last len(cols)-2
+            m = dict(zip(cols[2:], vals[-(len(cols) - 2):]))
+            try:
+                return (float(m["dram_read_MB"]) + float(m["dram_write_MB"])) * 1e6
+            except (KeyError, ValueError):
+                return None
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -513,7 +538,7 @@ def main():
     f_step = 3 * flops_per_update(d, chi, eta, kk, explicit, cbe=(scheme == "qr_cbe"))
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
-        "frac": achieved / dmma_peak if dmma_peak else None, "traffic": None,
+        "frac": achieved / dmma_peak if dmma_peak else None, "traffic": gemm_traffic(args.config),
         "kernel": "zgemm_kernel (mma.sync m8n8k4 f64 -> DMMA, TMA-staged): the hot-path contraction launches "
                   f"(>= {prof_min_flops:.3g} flops each: theta build, projections, Hastings, explicit error)",
         "peak_source": "FP64 DMMA microbenchmark (csrc/probe.cu) measured in this run; MEASURED_PEAKS.json has no FP64",
