@@ -53,7 +53,7 @@ __device__ __forceinline__ int rr_slot(int j, int r, int n) { return j == 0 ? 0 
 struct JacobiArgs {
   double2* G;     // N x N, row-major
   double2* V;     // N x N
-  double2* Jbuf;  // [npairs][32][32]
+  double2* Jbuf;  // [2 round parities][npairs][JX][JX]
   double* flags;  // [MAX_SWEEPS] per-sweep max |offdiag| (reduced per CTA into slots below)
   double* cta_max;  // [gridDim][2]
   unsigned* bar;
@@ -61,7 +61,8 @@ struct JacobiArgs {
   int full_inner;  // 1: full inner sweep in every outer round (QT_JACOBI_FULL)
   double tol;
   int* sweeps_out;
-  long long* prof;  // optional: cycles of CTA 0 in phase A / barrier / phase B / barrier
+  long long* prof;  // optional: cycles of CTA 0 in phase A / flag waits / phase B / first wave + barrier
+  unsigned* tflag;  // [P(P+1)/2] round counter of the last update of every G pair tile
   const double* fro2;  // ||G||_F^2 (device)
 };
 
@@ -205,7 +206,7 @@ __device__ __forceinline__ void tile_mm(double2 (*A)[JX + 1], bool conj_t, doubl
 template <int JB>
 __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   constexpr int JX = 2 * JB;   // subproblem size
-  constexpr int JT = JB * 16;  // threads: 16 x (JX/2) register blocks of 2 x JX/16
+  constexpr int JT = JB * 16;  // threads
   extern __shared__ double2 jdyn[];
   __shared__ Rot rots[JB];
   __shared__ int rp[JB], rq[JB];
@@ -216,187 +217,289 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   __shared__ int done_flag;
 
   const int tid = threadIdx.x;
-  const unsigned G = gridDim.x;
-  const int npairs = a.nb / 2;
+  const int G = static_cast<int>(gridDim.x);
+  const int cta = static_cast<int>(blockIdx.x);
+  const int nb = a.nb, P = nb / 2, R1 = nb - 1;  // pairs per round, rounds per sweep
   const int N = a.N;
+  const int ngt = P * (P + 1) / 2, nvt = (N / JX) * P;
   const double sc = jscale(a.fro2);
   const double abs_tol = 1e-22 * sqrt(*a.fro2) * sc;
   const double abs_tol2 = abs_tol * abs_tol, tol2 = a.tol * a.tol;
-  int sweep = 0;
-  long long pa = 0, pb1 = 0, pbB = 0, pb2 = 0;
+  const bool stamp = a.prof && tid == 0 && cta == 0;
+  long long pa = 0, pw = 0, pb = 0, ps = 0;
   unsigned epoch = 0;
+  double mx = 0.0;  // any rotation met the criterion in this CTA during the current sweep
 
-  for (; sweep < MAX_SWEEPS; ++sweep) {
-    double mx = 0.0;  // max |offdiag| met by this CTA during the sweep
-    for (int round = 0; round < a.nb - 1; ++round) {
-      long long tp0 = (a.prof && tid == 0 && blockIdx.x == 0) ? clock64() : 0;
-      // ---------------- phase A: 32x32 subproblems
-      for (int p = blockIdx.x; p < npairs; p += G) {
-        const int bI = rr_slot(p, round, a.nb), bJ = rr_slot(a.nb - 1 - p, round, a.nb);
-        // local index l < 16 -> bI*16 + l, else bJ*16 + l - 16
-        for (int e = tid; e < JX * JX; e += JT) {
-          const int i = e / JX, j = e % JX;
-          const int gi = (i < JB ? bI * JB + i : bJ * JB + i - JB);
-          const int gj = (j < JB ? bI * JB + j : bJ * JB + j - JB);
-          S[i][j] = a.G[static_cast<long long>(gi) * N + gj];
-          Jm[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-        }
-        __syncthreads();
-        // inner sweep over the 2JB local indices: JB "cross" rounds pairing
-        // I with J (i, JB + (i + s) mod JB), then JB-1 rounds inside I and J.
-        // The within-block rounds run only in the first outer round of a
-        // sweep (every block is paired there); later rounds of the sweep
-        // rotate the cross pairs only -- every pair is still rotated once per
-        // sweep.  Per inner round: JB threads form the rotations once, then
-        // the thread owning the 2x2 block (k,l) writes U_k^H S_kl U_l and
-        // J_kl U_l in place.
-        const int n_inner = (round == 0 || a.full_inner) ? JX - 1 : JB;
-        for (int ir = 0; ir < n_inner; ++ir) {
-          if (tid < JB) {
-            int p0, q0;
-            inner_pair(tid, ir, JB, p0, q0);
-            const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, S[p0][q0], tol2, abs_tol2);
-            if (rr.active) mx = 1.0;
-            rots[tid] = rr;
-            rp[tid] = p0;
-            rq[tid] = q0;
-          }
-          __syncthreads();
-          for (int b = tid; b < JB * JB; b += JT) {
-            const int k = b / JB, l = b % JB;
-            const Rot rk = rots[k], rl = rots[l];
-            if (!rk.active && !rl.active) continue;
-            const int pk = rp[k], qk = rq[k], pl = rp[l], ql = rq[l];
-            double2 s00 = S[pk][pl], s01 = S[pk][ql], s10 = S[qk][pl], s11 = S[qk][ql];
-            if (rk.active) rot_rows(s00, s01, s10, s11, rk);
-            if (rl.active) {
-              rot_cols(s00, s01, s10, s11, rl);
-              double2 j00 = Jm[pk][pl], j01 = Jm[pk][ql], j10 = Jm[qk][pl], j11 = Jm[qk][ql];
-              rot_cols(j00, j01, j10, j11, rl);
-              Jm[pk][pl] = j00;
-              Jm[pk][ql] = j01;
-              Jm[qk][pl] = j10;
-              Jm[qk][ql] = j11;
-            }
-            if (k == l) {  // the rotated pivot block is diagonal and real
-              s00.y = 0.0;
-              s11.y = 0.0;
-              if (rk.active) {
-                s01 = make_double2(0.0, 0.0);
-                s10 = make_double2(0.0, 0.0);
-              }
-            }
-            S[pk][pl] = s00;
-            S[pk][ql] = s01;
-            S[qk][pl] = s10;
-            S[qk][ql] = s11;
-          }
-          __syncthreads();
-        }
-        for (int e = tid; e < JX * JX; e += JT) a.Jbuf[static_cast<long long>(p) * JX * JX + e] = Jm[e / JX][e % JX];
-        __syncthreads();
-      }
-      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pa += t - tp0; tp0 = t; }
-      jgrid_sync(a.bar, G, epoch);
-      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pb1 += t - tp0; tp0 = t; }
-      // ---------------- phase B: tile updates of G and V
-      // G is Hermitian: only pair tiles xa <= yb are computed, the tile
-      // (yb, xa) is written as the conjugate transpose
-      const int nrowchunks = N / JX;
-      const int ngt = npairs * (npairs + 1) / 2;
-      const int ntiles = ngt + nrowchunks * npairs;
-      for (int t = blockIdx.x; t < ntiles; t += G) {
-        const bool isG = t < ngt;
-        int xa, yb, rc = 0;
-        if (isG) {
-          int u = t;
-          xa = 0;
-          while (u >= npairs - xa) {
-            u -= npairs - xa;
-            ++xa;
-          }
-          yb = xa + u;
-        } else {
-          const int u = t - ngt;
-          rc = u / npairs;
-          yb = u % npairs;
-          xa = -1;
-        }
-        const int yI = rr_slot(yb, round, a.nb), yJ = rr_slot(a.nb - 1 - yb, round, a.nb);
-        int xI = 0, xJ = 0;
-        if (isG) {
-          xI = rr_slot(xa, round, a.nb);
-          xJ = rr_slot(a.nb - 1 - xa, round, a.nb);
-        }
-        double2* M = isG ? a.G : a.V;
-        // load tile into S, J_Y into Jm
-        for (int e = tid; e < JX * JX; e += JT) {
-          const int i = e / JX, j = e % JX;
-          const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
-          const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
-          S[i][j] = M[static_cast<long long>(gi) * N + gj];
-          Jm[i][j] = a.Jbuf[static_cast<long long>(yb) * JX * JX + e];
-        }
-        __syncthreads();
-        // T1 = S Jy, then (G tiles) out = Jx^H T1, on the FP64 tensor pipe
-        tile_mm<JX, JT / 32>(S, false, Jm, T1);
-        __syncthreads();
-        if (isG) {
-          for (int e = tid; e < JX * JX; e += JT) Jm[e / JX][e % JX] = a.Jbuf[static_cast<long long>(xa) * JX * JX + e];
-          __syncthreads();
-          tile_mm<JX, JT / 32>(Jm, true, T1, S);
-          __syncthreads();
-        }
-        double2(*O)[JX + 1] = isG ? S : T1;
-        for (int e = tid; e < JX * JX; e += JT) {
-          const int i = e / JX, j = e % JX;
-          const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
-          const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
-          M[static_cast<long long>(gi) * N + gj] = O[i][j];
-        }
-        if (isG && xa != yb)
-          for (int e = tid; e < JX * JX; e += JT) {  // mirror, coalesced along i
-            const int j = e / JX, i = e % JX;
-            const int gi = i < JB ? xI * JB + i : xJ * JB + i - JB;
-            const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
-            M[static_cast<long long>(gj) * N + gi] = cconj(O[i][j]);
-          }
-        __syncthreads();
-      }
-      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pbB += t - tp0; tp0 = t; }
-      jgrid_sync(a.bar, G, epoch);
-      if (a.prof && tid == 0 && blockIdx.x == 0) { const long long t = clock64(); pb2 += t - tp0; }
+  // ---- round-robin bookkeeping: block at position j of round r; pair of a
+  // block in round r; the block paired with b in round r
+  auto pos_of = [&](int b, int r) {
+    if (b == 0) return 0;
+    int j = (b - 1 - r) % R1;
+    if (j < 0) j += R1;
+    return j + 1;
+  };
+  auto pair_of = [&](int b, int r) {
+    const int j = pos_of(b, r);
+    return j < P ? j : nb - 1 - j;
+  };
+  auto partner = [&](int b, int r) { return rr_slot(nb - 1 - pos_of(b, r), r, nb); };
+  auto tidx = [&](int x, int y) { return x * P - x * (x - 1) / 2 + (y - x); };  // x <= y
+
+  // ---- phase A: one 2JB x 2JB subproblem of round `round`, pair p -> Jbuf[p]
+  auto jslot = [&](long long g, int p) { return a.Jbuf + ((g & 1) * P + p) * static_cast<long long>(JX * JX); };
+  auto phase_a = [&](long long g, int round, int p) {
+    const int bI = rr_slot(p, round, nb), bJ = rr_slot(nb - 1 - p, round, nb);
+    for (int e = tid; e < JX * JX; e += JT) {
+      const int i = e / JX, j = e % JX;
+      const int gi = (i < JB ? bI * JB + i : bJ * JB + i - JB);
+      const int gj = (j < JB ? bI * JB + j : bJ * JB + j - JB);
+      S[i][j] = a.G[static_cast<long long>(gi) * N + gj];
+      Jm[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
     }
-    // ---------------- convergence: max over CTAs of the largest rotated element
+    __syncthreads();
+    // inner sweep over the 2JB local indices: JB "cross" rounds pairing I
+    // with J (i, JB + (i + s) mod JB), then JB-1 rounds inside I and J.  The
+    // within-block rounds run only in the first outer round of a sweep (every
+    // block is paired there); later rounds rotate the cross pairs only --
+    // every pair is still rotated once per sweep.  Per inner round: JB
+    // threads form the rotations once, then the thread owning the 2x2 block
+    // (k,l) writes U_k^H S_kl U_l and J_kl U_l in place.
+    const int n_inner = (round == 0 || a.full_inner) ? JX - 1 : JB;
+    for (int ir = 0; ir < n_inner; ++ir) {
+      if (tid < JB) {
+        int p0, q0;
+        inner_pair(tid, ir, JB, p0, q0);
+        const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, S[p0][q0], tol2, abs_tol2);
+        if (rr.active) mx = 1.0;
+        rots[tid] = rr;
+        rp[tid] = p0;
+        rq[tid] = q0;
+      }
+      __syncthreads();
+      for (int b = tid; b < JB * JB; b += JT) {
+        const int k = b / JB, l = b % JB;
+        const Rot rk = rots[k], rl = rots[l];
+        if (!rk.active && !rl.active) continue;
+        const int pk = rp[k], qk = rq[k], pl = rp[l], ql = rq[l];
+        double2 s00 = S[pk][pl], s01 = S[pk][ql], s10 = S[qk][pl], s11 = S[qk][ql];
+        if (rk.active) rot_rows(s00, s01, s10, s11, rk);
+        if (rl.active) {
+          rot_cols(s00, s01, s10, s11, rl);
+          double2 j00 = Jm[pk][pl], j01 = Jm[pk][ql], j10 = Jm[qk][pl], j11 = Jm[qk][ql];
+          rot_cols(j00, j01, j10, j11, rl);
+          Jm[pk][pl] = j00;
+          Jm[pk][ql] = j01;
+          Jm[qk][pl] = j10;
+          Jm[qk][ql] = j11;
+        }
+        if (k == l) {  // the rotated pivot block is diagonal and real
+          s00.y = 0.0;
+          s11.y = 0.0;
+          if (rk.active) {
+            s01 = make_double2(0.0, 0.0);
+            s10 = make_double2(0.0, 0.0);
+          }
+        }
+        S[pk][pl] = s00;
+        S[pk][ql] = s01;
+        S[qk][pl] = s10;
+        S[qk][ql] = s11;
+      }
+      __syncthreads();
+    }
+    double2* jo = jslot(g, p);  // double-buffered: round g+1's solves overlap round g's tile updates
+    for (int e = tid; e < JX * JX; e += JT) jo[e] = Jm[e / JX][e % JX];
+    __syncthreads();
+  };
+
+  // ---- phase B work item: G pair tile (xa <= yb) or V row chunk rc
+  auto tile = [&](long long g, int round, bool isG, int xa, int yb, int rc) {
+    const double2* jy = jslot(g, yb);
+    const double2* jx = jslot(g, xa < 0 ? 0 : xa);
+    const int yI = rr_slot(yb, round, nb), yJ = rr_slot(nb - 1 - yb, round, nb);
+    int xI = 0, xJ = 0;
+    if (isG) {
+      xI = rr_slot(xa, round, nb);
+      xJ = rr_slot(nb - 1 - xa, round, nb);
+    }
+    double2* M = isG ? a.G : a.V;
+    for (int e = tid; e < JX * JX; e += JT) {
+      const int i = e / JX, j = e % JX;
+      const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
+      const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
+      S[i][j] = M[static_cast<long long>(gi) * N + gj];
+      Jm[i][j] = jy[e];
+    }
+    __syncthreads();
+    // T1 = S Jy, then (G tiles) out = Jx^H T1, on the FP64 tensor pipe
+    tile_mm<JX, JT / 32>(S, false, Jm, T1);
+    __syncthreads();
+    if (isG) {
+      for (int e = tid; e < JX * JX; e += JT) Jm[e / JX][e % JX] = jx[e];
+      __syncthreads();
+      tile_mm<JX, JT / 32>(Jm, true, T1, S);
+      __syncthreads();
+    }
+    double2(*O)[JX + 1] = isG ? S : T1;
+    for (int e = tid; e < JX * JX; e += JT) {
+      const int i = e / JX, j = e % JX;
+      const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
+      const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
+      M[static_cast<long long>(gi) * N + gj] = O[i][j];
+    }
+    if (isG && xa != yb)
+      for (int e = tid; e < JX * JX; e += JT) {  // mirror, coalesced along i
+        const int j = e / JX, i = e % JX;
+        const int gi = i < JB ? xI * JB + i : xJ * JB + i - JB;
+        const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
+        M[static_cast<long long>(gj) * N + gi] = cconj(O[i][j]);
+      }
+    __syncthreads();
+  };
+  // publish a G tile of global round rg (release after the CTA's stores)
+  auto flag_tile = [&](int x, int y, unsigned rg) {
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tflag + tidx(x, y)), "r"(rg) : "memory");
+    }
+  };
+  auto wait_tile = [&](int x, int y, unsigned rg) {
+    if (tid == 0) {
+      const unsigned* f = a.tflag + tidx(min(x, y), max(x, y));
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      } while (v < rg);
+    }
+  };
+  // CTA-wide "any rotation this sweep" -> cta_max[sweep & 1][cta]; reset
+  auto publish = [&](int sweep) {
     red[tid] = mx;
     __syncthreads();
     for (int w = JT / 2; w > 0; w >>= 1) {
       if (tid < w) red[tid] = fmax(red[tid], red[tid + w]);
       __syncthreads();
     }
-    if (tid == 0) a.cta_max[(sweep & 1) * G + blockIdx.x] = red[0];
-    jgrid_sync(a.bar, G, epoch);
-    if (tid == 0) {  // converged: no rotation met the criterion in a whole sweep
-      double m = 0.0;
-      for (unsigned b = 0; b < G; ++b) m = fmax(m, __ldcg(&a.cta_max[(sweep & 1) * G + b]));
-      done_flag = m == 0.0;
+    if (tid == 0) a.cta_max[(sweep & 1) * G + cta] = red[0];
+    mx = 0.0;
+  };
+
+  // ---- schedule: phase A of round 0, barrier; then every iteration runs
+  // phase B of round (sw, rd) and, overlapped with it, phase A of the next
+  // round: the 2P pair tiles the next subproblems read (the diagonal tiles,
+  // CTA x, and one off-diagonal tile per next pair, CTAs P..) go first and are
+  // flagged; the CTAs < P wait for their three tiles and solve; the other
+  // CTAs finish the remaining tiles; one grid barrier per round.
+  if (cta < P) phase_a(0, 0, cta);
+  if (R1 == 1) publish(0);
+  jgrid_sync(a.bar, G, epoch);
+  int sw = 0, rd = 0;
+  for (;;) {
+    long long t0 = stamp ? clock64() : 0;
+    bool done = false;
+    if (rd == R1 - 1) {  // every phase A of sweep sw has run: converged if none rotated
+      if (tid == 0) {
+        double m = 0.0;
+        for (int b = 0; b < G; ++b) m = fmax(m, __ldcg(&a.cta_max[(sw & 1) * G + b]));
+        done_flag = m == 0.0;
+      }
+      __syncthreads();
+      done = done_flag != 0;
     }
-    __syncthreads();
-    if (done_flag) break;
+    const int ns = rd == R1 - 1 ? sw + 1 : sw, nr = rd == R1 - 1 ? 0 : rd + 1;
+    const bool doA = !done && ns < MAX_SWEEPS;
+    const long long gcur = static_cast<long long>(sw) * R1 + rd;  // global round index
+    const unsigned rg = static_cast<unsigned>(gcur + 1);
+    // critical off-diagonal tile of next pair q: the pairs (round rd) of its blocks
+    auto crit = [&](int q, int& x, int& y) {
+      const int u = pair_of(rr_slot(q, nr, nb), rd), v = pair_of(rr_slot(nb - 1 - q, nr, nb), rd);
+      x = min(u, v);
+      y = max(u, v);
+    };
+    auto is_crit = [&](int x, int y) {  // x < y
+      const int y1 = pair_of(partner(rr_slot(x, rd, nb), nr), rd);
+      const int y2 = pair_of(partner(rr_slot(nb - 1 - x, rd, nb), nr), rd);
+      return y == y1 || y == y2;
+    };
+    if (cta < P) {
+      tile(gcur, rd, true, cta, cta, 0);
+      if (doA) flag_tile(cta, cta, rg);
+    }
+    if (doA && cta >= P)
+      for (int q = cta - P; q < P; q += G - P) {
+        int x, y;
+        crit(q, x, y);
+        if (x == y) continue;
+        // two next pairs can read the same tile (blocks of pairs x and y
+        // pair up crosswise): the lower next pair owns it
+        const int b1 = rr_slot(q, nr, nb), b2 = rr_slot(nb - 1 - q, nr, nb);
+        const int o1 = b1 == rr_slot(pair_of(b1, rd), rd, nb) ? rr_slot(nb - 1 - pair_of(b1, rd), rd, nb)
+                                                                : rr_slot(pair_of(b1, rd), rd, nb);
+        const int o2 = partner(o1, nr);  // the other block of pair(b1) meets o2 in the next round
+        if (o2 != b2 && pair_of(o2, rd) == pair_of(b2, rd) && pair_of(o1, nr) < q) continue;
+        tile(gcur, rd, true, x, y, 0);
+        flag_tile(x, y, rg);
+      }
+    long long t1 = stamp ? clock64() : 0;
+    if (doA && cta < P) {
+      int x, y;
+      crit(cta, x, y);
+      wait_tile(x, x, rg);
+      wait_tile(y, y, rg);
+      if (x != y) wait_tile(x, y, rg);
+      __syncthreads();
+      long long t2 = stamp ? clock64() : 0;
+      phase_a(gcur + 1, nr, cta);
+      if (stamp) {
+        pw += t2 - t1;
+        pa += clock64() - t2;
+      }
+    }
+    // remaining work: off-diagonal G tiles that are not critical, then V chunks
+    const int c0 = doA ? P : 0, nw = doA ? G - P : G;
+    if (cta >= c0)
+      for (int u = cta - c0; u < ngt + nvt; u += nw) {
+        if (u < ngt) {
+          int v = u, x = 0;
+          while (v >= P - x) {
+            v -= P - x;
+            ++x;
+          }
+          const int y = x + v;
+          if (y == x || (doA && is_crit(x, y))) continue;
+          tile(gcur, rd, true, x, y, 0);
+        } else {
+          const int w2 = u - ngt;
+          tile(gcur, rd, false, -1, w2 % P, w2 / P);
+        }
+      }
+    if (stamp) pb += clock64() - t1;
+    if (doA && nr == R1 - 1) publish(ns);
+    if (!doA) {
+      sw = ns;
+      break;
+    }
+    long long t3 = stamp ? clock64() : 0;
+    jgrid_sync(a.bar, G, epoch);
+    if (stamp) ps += clock64() - t3 + (t1 - t0);
+    sw = ns;
+    rd = nr;
   }
-  if (blockIdx.x == 0 && tid == 0) *a.sweeps_out = sweep + 1;
-  if (a.prof && blockIdx.x == 0 && tid == 0) {
+  if (cta == 0 && tid == 0) *a.sweeps_out = sw;
+  if (stamp) {
     a.prof[0] = pa;
-    a.prof[1] = pb1;
-    a.prof[2] = pbB;
-    a.prof[3] = pb2;
+    a.prof[1] = pw;
+    a.prof[2] = pb;
+    a.prof[3] = ps;
   }
 }
 
 // pad: G_pad = [[G, 0], [0, diag(-(|G|+1) - i)]], V = I
 __global__ void jacobi_setup_kernel(const double2* __restrict__ h, int n, int N, const double* fro, double2* G,
-                                    double2* V, unsigned* bar) {
+                                    double2* V, unsigned* bar, unsigned* tflag, int ntflag) {
   if (blockIdx.x == 0 && threadIdx.x == 0) bar[0] = 0;
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < ntflag; i += blockDim.x) tflag[i] = 0;
   const double sc = jscale(fro);
   const double shift = -(sqrt(*fro) * sc + 1.0);
   const long long total = static_cast<long long>(N) * N;
@@ -477,17 +580,22 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   if (nb & 1) ++nb;
   const int N = nb * JB;
   const int npairs = nb / 2;
-  double2* G = e.cbuf(S_EIG_V, static_cast<size_t>(2) * N * N + static_cast<size_t>(npairs) * JX * JX);
+  double2* G = e.cbuf(S_EIG_V, static_cast<size_t>(2) * N * N + static_cast<size_t>(2) * npairs * JX * JX);
   double2* V = G + static_cast<size_t>(N) * N;
   double2* Jbuf = V + static_cast<size_t>(N) * N;
   double* fro = e.dscal + SC_TMP2;
   norm2(e, h, n, n, n, fro);
-  jacobi_setup_kernel<<<static_cast<int>(std::min<long long>(ceil_div(static_cast<long long>(N) * N, 256), 2048)), 256,
-                        0, e.stream>>>(h, static_cast<int>(n), N, fro, G, V, e.barrier + 8);
-  QT_LAUNCHED();
-  const int grid = std::min(e.num_sms, std::max(npairs, std::min(npairs * npairs + (N / JX) * npairs, e.num_sms)));
-  double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8);
+  // at least P + 1 CTAs: CTAs < P solve the next round's subproblems while
+  // the others finish the tile updates
+  const int ngt = npairs * (npairs + 1) / 2;
+  const int grid = std::min(e.num_sms, std::max(2 * npairs, std::min(ngt + (N / JX) * npairs, e.num_sms)));
+  if (grid <= npairs) throw Error(Err::capacity, "eigh: matrix too large for the cooperative Jacobi kernel");
+  double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8 + ngt / 2 + 1);
   int* sweeps = reinterpret_cast<int*>(cta_max + 2 * grid);
+  unsigned* tflag = reinterpret_cast<unsigned*>(cta_max + 2 * grid + 8);
+  jacobi_setup_kernel<<<static_cast<int>(std::min<long long>(ceil_div(static_cast<long long>(N) * N, 256), 2048)), 256,
+                        0, e.stream>>>(h, static_cast<int>(n), N, fro, G, V, e.barrier + 8, tflag, ngt);
+  QT_LAUNCHED();
   JacobiArgs a;
   a.G = G;
   a.V = V;
@@ -501,6 +609,7 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   static const bool full_inner = std::getenv("QT_JACOBI_FULL") != nullptr;
   a.full_inner = full_inner ? 1 : 0;
   a.sweeps_out = sweeps;
+  a.tflag = tflag;
   static long long* prof = nullptr;
   if (std::getenv("QT_EIGH_DEBUG") && !prof) QT_CUDA(cudaMalloc(&prof, 8 * sizeof(long long)));
   a.prof = prof;
@@ -542,8 +651,8 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
     QT_CUDA(cudaMemcpy(pc, prof, sizeof(pc), cudaMemcpyDeviceToHost));
     const double rounds = static_cast<double>(sw) * (nb - 1);
     std::fprintf(stderr,
-                 "eigh n=%lld N=%d grid=%d sweeps=%d rounds/sweep=%d time=%.3f ms | cycles/round: A %.0f sync %.0f B %.0f "
-                 "sync %.0f\n",
+                 "eigh n=%lld N=%d grid=%d sweeps=%d rounds/sweep=%d time=%.3f ms | CTA 0 cycles/round: phase A %.0f "
+                 "flag wait %.0f phase B %.0f first wave + barrier %.0f\n",
                  n, N, grid, sw, nb - 1, ms, pc[0] / rounds, pc[1] / rounds, pc[2] / rounds, pc[3] / rounds);
     cudaEventDestroy(d0);
     cudaEventDestroy(d1);
