@@ -671,11 +671,92 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   QT_LAUNCHED();
 }
 
+namespace {
+// any nonzero off-diagonal element of the p x q matrix -> flag = 1
+__global__ void offdiag_any_kernel(const double2* __restrict__ m, long long p, long long q, int* flag) {
+  const long long total = p * q;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / q, j = e % q;
+    if (i != j) {
+      const double2 v = m[e];
+      if (v.x != 0.0 || v.y != 0.0) {
+        *flag = 1;
+        return;
+      }
+    }
+  }
+}
+
+// s = |diag(m)| sorted descending (ties: lower index first), one CTA bitonic
+__global__ void diag_sv_kernel(const double2* __restrict__ m, long long q, int k, double* s) {
+  extern __shared__ unsigned char dsm[];
+  int P = 1;
+  while (P < k) P <<= 1;
+  double* key = reinterpret_cast<double*>(dsm);
+  int* idx = reinterpret_cast<int*>(key + P);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    key[i] = i < k ? hypot(m[static_cast<long long>(i) * q + i].x, m[static_cast<long long>(i) * q + i].y) : -1.0;
+    idx[i] = i;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          const bool i_first = (key[i] > key[j]) || (key[i] == key[j] && idx[i] < idx[j]);
+          if (desc != i_first) {
+            const double tk = key[i];
+            key[i] = key[j];
+            key[j] = tk;
+            const int ti = idx[i];
+            idx[i] = idx[j];
+            idx[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s[i] = key[i];
+}
+}  // namespace
+
+bool diagonal_singular_values(Engine& e, const double2* m, long long p, long long q, double* s) {
+  // CBE bond matrices are diagonal (gates.cpp:430, diagonal_bond_matrix): their
+  // Schmidt values are the sorted |diagonal| -- exact, no Gram route
+  const long long k = std::min(p, q);
+  if (k <= 0 || k > 16384) return false;
+  int* flag = reinterpret_cast<int*>(e.dscal + SC_TMP3);
+  QT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), e.stream));
+  offdiag_any_kernel<<<static_cast<int>(std::min<long long>(ceil_div(p * q, 256), 4 * e.num_sms)), 256, 0,
+                       e.stream>>>(m, p, q, flag);
+  QT_LAUNCHED();
+  int h = 1;
+  QT_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  if (h != 0) return false;
+  int P = 1;
+  while (P < k) P <<= 1;
+  const size_t smem = static_cast<size_t>(P) * (sizeof(double) + sizeof(int));
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    QT_CUDA(cudaFuncSetAttribute(diag_sv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = smem;
+  }
+  diag_sv_kernel<<<1, 1024, smem, e.stream>>>(m, q, static_cast<int>(k), s);
+  QT_LAUNCHED();
+  return true;
+}
+
 double* singular_values_device(Engine& e, const double2* m, long long p, long long q) {
   // s = sqrt(max(eig(m^H m), 0)) (Gram route, absolute accuracy ~ sqrt(u) s_0
   // for the smallest values), descending; returned in the S_EIG_W slot
   const long long k = std::min(p, q);
   if (k == 0) return e.dbuf(S_EIG_W, 8);
+  double* wd = e.dbuf(S_EIG_W, k + 8);
+  if (diagonal_singular_values(e, m, p, q, wd)) return wd;
   const bool wide = q > p;  // Gram on the smaller side
   const long long g = wide ? p : q;
   double2* gm = e.cbuf(S_GRAM, g * g);

@@ -64,6 +64,23 @@ def test_schmidt_values_match_svd(ctx, p, qq):
     assert np.max(np.abs(s ** 2 - s_ref ** 2)) <= 1e-13 * np.sum(s_ref ** 2)
 
 
+@pytest.mark.parametrize("p,qq", [(1, 1), (7, 7), (300, 300), (12, 20)])
+def test_schmidt_values_of_diagonal_bond_are_exact(ctx, p, qq):
+    """CBE bond matrices are diagonal (gates.cpp:430): the spectrum is the
+    sorted |diagonal| (SURVEY.md §8 a13 fast path) to the rounding of |z|,
+    tiny values included -- no Gram-route noise."""
+    rng = np.random.default_rng(p * 31 + qq)
+    k = min(p, qq)
+    mags = np.exp(-rng.uniform(0, 40, k))
+    mags[k // 2:k // 2 + 1] = mags[0]  # a tie
+    m = np.zeros((p, qq), dtype=complex)
+    m[np.arange(k), np.arange(k)] = mags * np.exp(1j * rng.uniform(0, 2 * np.pi, k))
+    s = q.schmidt_values_of(m, ctx)
+    ref_s = np.sort(np.abs(np.diag(m)))[::-1]
+    assert s.shape == ref_s.shape
+    assert np.max(np.abs(s - ref_s) / ref_s) <= 4.5e-16  # 2 ulp: device vs host hypot
+
+
 def random_inputs(d, chi, seed):
     rng = np.random.default_rng(seed)
     bm = ref.random_right_isometry(rng, d, chi, chi)
