@@ -571,6 +571,13 @@ def main():
         line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                                 "sample": f"{n} Trotter steps ({dt:.1f} s) of the NumPy/LAPACK oracle on the same "
                                           f"config, OpenBLAS threads = {os.cpu_count()}"}
+        # the reference's SVD-TEBD comparator (gates.cpp:312-322) on the same cell
+        # and truncation, timed beside it
+        cfg_svd = (cfg[0], cfg[1], cfg[2], "svd", cfg[4], cfg[5])
+        rate_s, n_s, dt_s = cpu_reference_rate(cfg_svd, budget_s=max(1.0, args.cpu_budget / 3))
+        line["cpu_baseline_svd"] = {"value": rate_s, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"{n_s} Trotter steps ({dt_s:.1f} s) of the oracle's SVD-TEBD update "
+                                              "(zgesdd of theta) on the same state and gate schedule"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if graph_path:
