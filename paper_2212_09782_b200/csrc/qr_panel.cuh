@@ -148,8 +148,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
   double2* Ts = ctws + NB;                   // [32][32]   T factor (CTA 0)
   double2* Z = Ts + NB * NB;                 // [32][32]   z vectors of the T recurrence (CTA 0)
   double2* taus = Z + NB * NB;               // [32]
-  Reflector* refl = reinterpret_cast<Reflector*>(taus + NB);   // (3 x double2)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(taus + NB + 3);  // [2]
+  double2* scales = taus + NB;               // [32]       reflector scales (CTA 0)
+  Reflector* refl = reinterpret_cast<Reflector*>(scales + NB);   // (3 x double2)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scales + NB + 3);  // [2]
 
   const int w = threadIdx.x >> 5, k = threadIdx.x & 31;
   const unsigned rank = cluster_rank();
@@ -237,13 +238,13 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
       // conj(tau) w_k, w_k = a_ck + conj(scale) s_k (zero on lanes that keep their column)
       ctws[k] = (k > c && k < nbp) ? cmul(cconj(Rw.tau), cadd(dk, cmul(cconj(Rw.scale), sk)))
                                    : make_double2(0.0, 0.0);
-      // z vector of the T recurrence (zlarft), l < c:
-      //   z_l = -tau (conj(v_c,l) + scale h_l),  v_c,l = scale_l x^(l)_c,  h_l = conj(scale_l) conj(p_l)
-      if (rank == 0)
-        Z[c * NB + k] = (k < c) ? cmul(make_double2(-Rw.tau.x, -Rw.tau.y),
-                                       cadd(cconj(cmul(my_scale, dk)),
-                                            cmul(Rw.scale, cmul(cconj(my_scale), cconj(sk)))))
-                                : make_double2(0.0, 0.0);
+      // inputs of the z vector of the T recurrence, formed after the loop
+      // (off the per-column chain): row c and the partials of column c
+      if (rank == 0) {
+        Z[c * NB + k] = dk;
+        Ts[c * NB + k] = sk;
+        if (k == 0) scales[c] = Rw.scale;
+      }
       if (a.dbg && rank == 0 && k == 0) a.dbg[c * 8 + 6] = clock64();
     }
     __syncthreads();
@@ -308,6 +309,15 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
     }
   }
   if (rank != 0) return;
+  // z vectors of the T recurrence (zlarft), l < c (all scales are final):
+  //   z_l = -tau_c (conj(v_c,l) + scale_c h_l),  v_c,l = scale_l x^(l)_c,  h_l = conj(scale_l) conj(p_l)
+  for (int c = w; c < nbp; c += CL_WARPS) {
+    const double2 dk = Z[c * NB + k], sk = Ts[c * NB + k], tc = taus[c], scl = scales[c];
+    Z[c * NB + k] = (k < c) ? cmul(make_double2(-tc.x, -tc.y), cadd(cconj(cmul(my_scale, dk)),
+                                                                   cmul(scl, cmul(cconj(my_scale), cconj(sk)))))
+                            : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
   // zlarft (forward, columnwise) on CTA 0: T[c,c] = tau_c, T[0:c,c] = T[0:c,0:c] z_c;
   // each column's triangular product is spread over the 16 warps
   for (int e = threadIdx.x; e < NB * NB; e += CL_THREADS) Ts[e] = make_double2(0.0, 0.0);
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
 }
 
 constexpr size_t panel_cluster_smem(int rpw) {
-  return (size_t(2 * CL_WARPS * rpw) + CL_WARPS * NB + 2 * 16 * NB + 6 * NB + NB + 2 * NB * NB + NB + 3) *
+  return (size_t(2 * CL_WARPS * rpw) + CL_WARPS * NB + 2 * 16 * NB + 6 * NB + NB + 2 * NB * NB + 2 * NB + 3) *
              sizeof(double2) +
          2 * 8;
 }
