@@ -9,6 +9,7 @@
 // per buffer-parity pattern and replayed as one graph launch: no host work and
 // no launch gaps inside the step.  The report scalars of every update are
 // copied into pinned host memory inside the graph.
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -36,6 +37,13 @@ struct UniformDev {
   };
   std::map<std::string, GraphEntry> graphs;
   std::map<std::string, int> seen;
+  // L >= 4: the L/2 updates of a layer are independent
+  // (proj/tests/test_tebd.cc:139-175); update j of a layer runs on engine j
+  // (0 = the context's own), each with its own stream and workspace; the
+  // streams fork from and join into the main stream around every layer
+  // (inside a captured graph the fork/join become graph dependencies)
+  std::vector<Engine*> aux;
+  std::vector<cudaEvent_t> ev;
 
   long long site_elems(int m) const { return d * chi[m] * chi[(m + 1) % L]; }
   long long bond_elems(int m) const { return chi[m] * chi[m]; }
@@ -91,6 +99,11 @@ UniformDev* uniform_create(Engine& e, int L, long long d, const std::vector<long
 void uniform_destroy(UniformDev* s) {
   if (!s) return;
   cudaStreamSynchronize(s->e->stream);
+  for (Engine* a : s->aux) {
+    a->destroy();
+    delete a;
+  }
+  for (cudaEvent_t x : s->ev) cudaEventDestroy(x);
   for (auto& kv : s->graphs) {
     cudaGraphExecDestroy(kv.second.exec);
     for (auto& r : kv.second.prof) {
@@ -158,10 +171,56 @@ std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<
     out[k].bond = ups[k].n;
     out[k].before = out[k].eta = out[k].after = s->chi[ups[k].n];
   }
+  // layer boundaries in `ups` and the engine of every update
+  std::vector<size_t> layer_start;
+  {
+    size_t k = 0;
+    for (const auto& ly : layers) {
+      layer_start.push_back(k);
+      for (int m = ly.first; m < L; m += 2) ++k;
+    }
+    layer_start.push_back(k);
+  }
+  const bool concurrent = scheme_qr && L >= 4 && std::getenv("QT_UNIFORM_SERIAL") == nullptr;
+  if (concurrent) {
+    const size_t need = static_cast<size_t>(L / 2 - 1);
+    while (s->aux.size() < need) {
+      Engine* a = new Engine;
+      a->init(e.device, nullptr);
+      s->aux.push_back(a);
+    }
+    while (s->ev.size() < 2 * (need + 1)) {
+      cudaEvent_t x;
+      QT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+      s->ev.push_back(x);
+    }
+  }
+  auto engine_of = [&](size_t k) -> Engine& {
+    if (!concurrent) return e;
+    size_t ly = 0;
+    while (layer_start[ly + 1] <= k) ++ly;
+    const size_t j = k - layer_start[ly];
+    return j == 0 ? e : *s->aux[j - 1];
+  };
+  auto fork = [&](size_t nj) {  // aux streams 0..nj-2 wait for the main stream
+    if (!concurrent || nj < 2) return;
+    QT_CUDA(cudaEventRecord(s->ev[0], e.stream));
+    for (size_t j = 1; j < nj; ++j) QT_CUDA(cudaStreamWaitEvent(s->aux[j - 1]->stream, s->ev[0], 0));
+  };
+  auto join = [&](size_t nj) {  // the main stream waits for the aux streams
+    if (!concurrent || nj < 2) return;
+    for (size_t j = 1; j < nj; ++j) {
+      QT_CUDA(cudaEventRecord(s->ev[j], s->aux[j - 1]->stream));
+      QT_CUDA(cudaStreamWaitEvent(e.stream, s->ev[j], 0));
+    }
+  };
   auto run_updates = [&](bool eager) {
     std::vector<int> sact = s->sact, bact = s->bact;
+    size_t ly = 0;
     for (size_t k = 0; k < nup; ++k) {
+      if (k == layer_start[ly]) fork(layer_start[ly + 1] - layer_start[ly]);
       const Upd& u = ups[k];
+      Engine& eu = engine_of(k);
       const int m = u.m, n = u.n, nr = (n + 1) % L;
       Dims D{s->d, s->chi[m], s->chi[m], s->chi[n], s->chi[nr]};
       const double2* xi = s->bbuf[bact[m]][m];
@@ -179,8 +238,9 @@ std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<
       out[k].before = D.chi_n;
       if (scheme_qr) {
         const long long eta = qr_eta(pol, D);
-        gate_qr_async(e, D, xi, bm, bn, u.u, pol, eta, outputs(eta));
-        QT_CUDA(cudaMemcpyAsync(s->rep_dev + 8 * k, e.dscal, 8 * sizeof(double), cudaMemcpyDeviceToDevice, e.stream));
+        gate_qr_async(eu, D, xi, bm, bn, u.u, pol, eta, outputs(eta));
+        QT_CUDA(cudaMemcpyAsync(s->rep_dev + 8 * k, eu.dscal, 8 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                eu.stream));
         out[k].eta = out[k].after = eta;
         if (eager) s->chi[n] = eta;
       } else {
@@ -196,6 +256,10 @@ std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<
       if (eager) {
         s->sact = sact;
         s->bact = bact;
+      }
+      if (k + 1 == layer_start[ly + 1]) {
+        join(layer_start[ly + 1] - layer_start[ly]);
+        ++ly;
       }
     }
     if (scheme_qr)

@@ -60,3 +60,46 @@ def test_device_state_grows_bond_dimension_eagerly(ctx):
     snap = dev.snapshot()
     for s in range(2):
         assert abs(q.expectation_local(snap, z, s, ctx) - ref.expectation_local(st_o, z, s)) < 1e-10
+
+
+def random_state_L(ctx, d, chi, L, seed):
+    rng = np.random.default_rng(seed)
+    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(L)]
+    bonds = []
+    for _ in range(L):
+        x = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+        bonds.append(x / np.linalg.norm(x))
+    return q.UniformMPS.from_numpy(ctx, d, sites, bonds)
+
+
+@pytest.mark.parametrize("L", [4, 6])
+def test_concurrent_same_parity_updates_bitwise_equal_serial(ctx, L):
+    """L >= 4: the L/2 updates of a layer run on concurrent streams (one
+    engine each, fork/join per layer); graph-replayed and
+    eager steps are bitwise those of the one-stream value path."""
+    d, chi = 3, 24
+    sched = model.trotter_schedule(model.bond_hamiltonian(d, 2.0), 0.05, 2)
+    gates = [(p, ctx.tensor(g)) for p, g in sched]
+    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0)
+    st = random_state_L(ctx, d, chi, L, 5 + L)
+    ref_state = st
+    dev_g = q.DeviceUniformMPS(st, ctx)
+    dev_e = q.DeviceUniformMPS(st, ctx)
+    for _ in range(4):
+        ref_state, _ = q.tebd_step(ref_state, gates, "qr", pol, ctx)
+        dev_g.step(gates, "qr", pol, use_graph=True)
+        dev_e.step(gates, "qr", pol, use_graph=False)
+        for m in range(L):
+            v = ref_state.site_tensors[m].numpy()
+            assert np.array_equal(dev_g.view("site", m).numpy(), v)
+            assert np.array_equal(dev_e.view("site", m).numpy(), v)
+            assert np.array_equal(dev_g.view("bond", m).numpy(), ref_state.bond_matrices[m].numpy())
+    # and the oracle agrees on a gauge-invariant quantity
+    st_o = ref.UniformMPS(d, [t.numpy() for t in st.site_tensors], [b.numpy() for b in st.bond_matrices])
+    for _ in range(4):
+        st_o, _ = ref.tebd_step_uniform(st_o, sched, "qr", ref.TruncationPolicy(chi_max=chi, delta_chi_abs=0,
+                                                                                delta_chi_rel=0.0))
+    z = model.clock_operators(d)[0]
+    snap = dev_g.snapshot()
+    for s in range(L):
+        assert abs(q.expectation_local(snap, z, s, ctx) - ref.expectation_local(st_o, z, s)) < 1e-10
