@@ -59,7 +59,14 @@ class ShardedChain:
     """The sites [start, end) of an open chain owned by this rank."""
 
     def __init__(self, sites: Sequence, bonds: Sequence, n_sites: int, rank: int, world: int, backend,
-                 dist=None):
+                 dist=None, periodic: bool = False):
+        # periodic: a uniform unit cell of n_sites (even) sites whose odd layer
+        # includes the wrap bond (n-1, 0) (proj/src/gates.cpp:524-537); the
+        # blocks form a ring and the last rank's straddling bond is the wrap
+        # (SURVEY.md §8(e), uniform large unit cell)
+        if periodic and n_sites % 2:
+            raise ValueError("a periodic (uniform) cell needs an even number of sites")
+        self.periodic = periodic
         self.n = n_sites
         self.rank = rank
         self.world = world
@@ -105,14 +112,18 @@ class ShardedChain:
     def layer(self, parity: int, gates: Sequence, device="cpu"):
         """One Trotter layer: bonds (m, m+1) with m % 2 == parity; gates[m] acts on (m, m+1)."""
         start, end = self.start, self.end
-        has_right_straddle = parity == 1 and self.rank + 1 < self.world and end < self.n
-        has_left_straddle = parity == 1 and self.rank > 0
+        if self.periodic:
+            has_right_straddle = has_left_straddle = parity == 1 and self.world > 1
+        else:
+            has_right_straddle = parity == 1 and self.rank + 1 < self.world and end < self.n
+            has_left_straddle = parity == 1 and self.rank > 0
+        right, left = (self.rank + 1) % self.world, (self.rank - 1) % self.world
         pending = []
         # the right neighbour's first site is the right half of our straddling bond
         if has_left_straddle:
-            reqs, keep = self._send_tensor(self.sites[start], self.rank - 1)
+            reqs, keep = self._send_tensor(self.sites[start], left)
             pending.append((reqs, keep))
-        right_hdr = self._post_header(self.rank + 1, device) if has_right_straddle else None
+        right_hdr = self._post_header(right, device) if has_right_straddle else None
         # interior bonds of this parity (overlap the neighbour's transfer)
         interior = list(range(start + parity, end - 1, 2))
         if self.workers and len(interior) > 1:
@@ -120,19 +131,27 @@ class ShardedChain:
         else:
             for m in interior:
                 self._update(m, m + 1, gates[m])
-        # the straddling bond (end-1, end): owned here, results returned
+        # the wrap bond of a one-rank periodic cell is local
+        if self.periodic and parity == 1 and self.world == 1:
+            m = self.n - 1
+            bm, xi, bn, rep = self.be.apply(self.bonds[m], self.sites[m], self.sites[0], gates[m])
+            self.sites[m] = bm
+            self.bonds[0] = xi
+            self.sites[0] = bn
+            self.reports.append((0, rep))
+        # the straddling bond (end-1, end mod n): owned here, results returned
         if has_right_straddle:
-            right_site = self._recv_tensor(self.rank + 1, device, right_hdr)
+            right_site = self._recv_tensor(right, device, right_hdr)
             m = end - 1
             bm, xi, bn, rep = self.be.apply(self.bonds[m], self.sites[m], right_site, gates[m])
             self.sites[m] = bm
-            self.reports.append((m + 1, rep))
+            self.reports.append(((m + 1) % self.n, rep))
             for t in (xi, bn):
-                reqs, keep = self._send_tensor(t, self.rank + 1)
+                reqs, keep = self._send_tensor(t, right)
                 pending.append((reqs, keep))
         if has_left_straddle:
-            self.bonds[start] = self._recv_tensor(self.rank - 1, device)
-            self.sites[start] = self._recv_tensor(self.rank - 1, device)
+            self.bonds[start] = self._recv_tensor(left, device)
+            self.sites[start] = self._recv_tensor(left, device)
         for reqs, _ in pending:
             for r in reqs:
                 r.wait()

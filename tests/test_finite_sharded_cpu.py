@@ -134,3 +134,71 @@ def test_concurrent_bond_updates_match_sequential(workers):
         assert np.array_equal(a.sites[m], b.sites[m])
         assert np.array_equal(a.bonds[m], b.bonds[m])
     assert [[m for m, _ in r] for r in ra] == [[m for m, _ in r] for r in rb]
+
+
+def ring_state(L, d, chi, seed):
+    rng = np.random.default_rng(seed)
+    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(L)]
+    bonds = []
+    for _ in range(L):
+        x = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+        bonds.append(x / np.linalg.norm(x))
+    return sites, bonds
+
+
+def ring_worker(rank, world, port, L, d, chi, steps, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pol = ref.TruncationPolicy(chi_max=chi, sv_cutoff=1e-14)
+    sites, bonds = ring_state(L, d, chi, 17)
+    s, e = partition(L, world)[rank]
+
+    def apply(xi, bm, bn, u):
+        upd = ref.apply_gate_qr(xi, bm, bn, u, pol)
+        return upd.b_m, upd.xi_n, upd.b_n, upd.report
+
+    try:
+        chain = ShardedChain(sites[s:e], bonds[s:e], L, rank, world, numpy_backend(apply), dist, periodic=True)
+        gate_layers = [(0 if p == "even" else 1, [g] * L)
+                       for p, g in ref.trotter_schedule(ref.bond_hamiltonian(d, 2.0), 0.05, 2)]
+        for _ in range(steps):
+            chain.step(gate_layers)
+        out_q.put((rank, {m: chain.sites[m] for m in chain.sites}, {m: chain.bonds[m] for m in chain.bonds}))
+    except Exception as exc:
+        out_q.put((rank, repr(exc), None))
+        raise
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,world", [(8, 2), (8, 3), (6, 1)])
+def test_sharded_uniform_cell_ring_matches_oracle(L, world):
+    """Uniform large unit cell sharded over ranks as a ring (the last rank's
+    straddling bond is the wrap bond (L-1, 0)): bitwise equal to the oracle's
+    tebd_step(UniformMPS), proj/src/gates.cpp:513-540."""
+    d, chi, steps = 2, 4, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=ring_worker, args=(r, world, port, L, d, chi, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for r, s, b in results:
+        assert b is not None, f"rank {r} failed: {s}"
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sites, bonds = {}, {}
+    for _, s, b in results:
+        sites.update(s)
+        bonds.update(b)
+    s0, b0 = ring_state(L, d, chi, 17)
+    st = ref.UniformMPS(d, s0, b0)
+    sched = ref.trotter_schedule(ref.bond_hamiltonian(d, 2.0), 0.05, 2)
+    for _ in range(steps):
+        st, _ = ref.tebd_step_uniform(st, sched, "qr", ref.TruncationPolicy(chi_max=chi, sv_cutoff=1e-14))
+    for m in range(L):
+        assert np.array_equal(sites[m], st.site_tensors[m]), m
+        assert np.array_equal(bonds[m], st.bond_matrices[m]), m
