@@ -13,6 +13,7 @@
 #ifndef QRTEBD_B200_HPP
 #define QRTEBD_B200_HPP
 
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstddef>
@@ -322,6 +323,45 @@ inline double entropy_from_schmidt(const std::vector<double>& values) {
 
 inline double entanglement_entropy(Context& ctx, const UniformMPS& mps, std::size_t bond) {
   return entropy_from_schmidt(schmidt_values(ctx, mps, bond));
+}
+
+// proj/include/qrtebd/mps.hpp:40-53
+struct IsometryReport {
+  std::vector<double> right_defects, left_defects, translation_defects, norm_defects;
+  double max_right_defect = 0.0, max_left_defect = 0.0, max_translation_defect = 0.0, max_norm_defect = 0.0;
+  bool pass = false;
+  double max_defect() const {
+    return std::max(std::max(max_right_defect, max_left_defect), std::max(max_translation_defect, max_norm_defect));
+  }
+};
+
+// check_isometric(UniformMPS, tol), proj/src/mps.cpp:105-141
+inline IsometryReport check_isometric(Context& ctx, const UniformMPS& mps, double tol) {
+  const std::size_t L = mps.cell_length();
+  std::vector<DeviceTensor> s, b;
+  std::vector<qt_tensor*> sh(L), bh(L);
+  for (std::size_t m = 0; m < L; ++m) {
+    s.emplace_back(ctx, mps.site_tensors[m]);
+    b.emplace_back(ctx, mps.bond_matrices[m]);
+  }
+  for (std::size_t m = 0; m < L; ++m) {
+    sh[m] = s[m].get();
+    bh[m] = b[m].get();
+  }
+  IsometryReport r;
+  r.right_defects.resize(L);
+  r.left_defects.resize(L);
+  r.translation_defects.resize(L);
+  r.norm_defects.resize(L);
+  qt_isometry_report c{};
+  check(qt_check_isometric_uniform(ctx.get(), L, sh.data(), bh.data(), tol, r.right_defects.data(),
+                                   r.left_defects.data(), r.translation_defects.data(), r.norm_defects.data(), &c));
+  r.max_right_defect = c.max_right_defect;
+  r.max_left_defect = c.max_left_defect;
+  r.max_translation_defect = c.max_translation_defect;
+  r.max_norm_defect = c.max_norm_defect;
+  r.pass = c.pass != 0;
+  return r;
 }
 
 }  // namespace qrtebd

@@ -197,6 +197,23 @@ qt_status qt_schmidt_values(qt_ctx* ctx, const qt_tensor* xi, double* out, uint6
 qt_status qt_eigh(qt_ctx* ctx, const qt_tensor* h, double* w_host, qt_tensor** v_out);
 /* right_defect, mps.cpp:34-36: || sum_i B^i B^i^H - 1 ||_max */
 qt_status qt_right_defect(qt_ctx* ctx, const qt_tensor* b, double* out);
+/* check_isometric(UniformMPS, tol), proj/src/mps.cpp:105-141 (IsometryReport,
+ * proj/include/qrtebd/mps.hpp:40-53): per site the right defect; per bond the
+ * cell fixed-point ("left") and translation defects of the left weight
+ * lambda = Xi^T conj(Xi) and | ||Xi|| - 1 |.  Each per-index array (length
+ * cell_length) may be NULL; pass = max defect <= tol. */
+typedef struct qt_isometry_report {
+  double max_right_defect;
+  double max_left_defect;
+  double max_translation_defect;
+  double max_norm_defect;
+  int32_t pass;
+  int32_t reserved;
+} qt_isometry_report;
+qt_status qt_check_isometric_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* const* sites,
+                                     qt_tensor* const* bonds, double tol, double* right_defects,
+                                     double* left_defects, double* translation_defects, double* norm_defects,
+                                     qt_isometry_report* out);
 /* Bond energy <theta0|h|theta0>/<theta0|theta0>, theta0 = Xi B^m B^n
  * (an extension, not in the reference). */
 qt_status qt_bond_energy(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m, const qt_tensor* b_n,

@@ -52,6 +52,17 @@ class qt_bond_report(C.Structure):
     _fields_ = [("bond", C.c_uint64), ("report", qt_report)]
 
 
+class qt_isometry_report(C.Structure):
+    _fields_ = [
+        ("max_right_defect", C.c_double),
+        ("max_left_defect", C.c_double),
+        ("max_translation_defect", C.c_double),
+        ("max_norm_defect", C.c_double),
+        ("pass_", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
 P = C.c_void_p
 PP = C.POINTER(C.c_void_p)
 U64P = C.POINTER(C.c_uint64)
@@ -98,6 +109,7 @@ SIGNATURES = {
     "qt_expectation_local": (C.c_int, [P, P, P, P, DP]),
     "qt_schmidt_values": (C.c_int, [P, P, DP, U64P]),
     "qt_right_defect": (C.c_int, [P, P, DP]),
+    "qt_check_isometric_uniform": (C.c_int, [P, C.c_uint64, PP, PP, C.c_double, DP, DP, DP, DP, P]),
     "qt_eigh": (C.c_int, [P, P, DP, PP]),
     "qt_bond_energy": (C.c_int, [P, P, P, P, P, DP]),
     "qt_fp64_peak": (C.c_int, [P, C.c_int, DP]),

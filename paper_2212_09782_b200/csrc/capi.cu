@@ -1,5 +1,6 @@
 // extern "C" boundary (include/qrtebd_c.h).  Thin: validates shapes with the
 // reference's error taxonomy, allocates output handles, calls the engine.
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -827,6 +828,51 @@ qt_status qt_right_defect(qt_ctx* ctx, const qt_tensor* b, double* out) {
     require(ctx && b && out, qt::Err::input, "qt_right_defect: null argument");
     require_tensor(b, 3, "right_defect");
     *out = qt::right_defect(ctx->eng, b->data, b->shape[0], b->shape[1], b->shape[2]);
+  });
+}
+
+qt_status qt_check_isometric_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* const* sites,
+                                     qt_tensor* const* bonds, double tol, double* right_defects,
+                                     double* left_defects, double* translation_defects, double* norm_defects,
+                                     qt_isometry_report* out) {
+  return guard([&] {
+    require(ctx && sites && bonds && out && cell_length > 0, qt::Err::input,
+            "qt_check_isometric_uniform: null argument");
+    const uint64_t L = cell_length;
+    std::vector<const double2*> s(L), b(L);
+    std::vector<long long> chi(L);
+    long long d = 0;
+    for (uint64_t m = 0; m < L; ++m) {
+      require_tensor(sites[m], 3, "check_isometric");
+      require_tensor(bonds[m], 2, "check_isometric");
+      chi[m] = static_cast<long long>(bonds[m]->shape[0]);
+      if (m == 0) d = static_cast<long long>(sites[0]->shape[0]);
+    }
+    for (uint64_t m = 0; m < L; ++m) {
+      const uint64_t n = (m + 1) % L;
+      if (bonds[m]->shape[1] != bonds[m]->shape[0] || static_cast<long long>(sites[m]->shape[0]) != d ||
+          static_cast<long long>(sites[m]->shape[1]) != chi[m] ||
+          static_cast<long long>(sites[m]->shape[2]) != chi[n])
+        throw qt::Error(qt::Err::shape, "check_isometric: site/bond dimensions do not chain");
+      s[m] = sites[m]->data;
+      b[m] = bonds[m]->data;
+    }
+    const qt::IsometryParts r = qt::check_isometric_uniform(ctx->eng, d, chi, s, b);
+    auto mx = [](const std::vector<double>& v) { return v.empty() ? 0.0 : *std::max_element(v.begin(), v.end()); };
+    out->max_right_defect = mx(r.right);
+    out->max_left_defect = mx(r.left);
+    out->max_translation_defect = mx(r.translation);
+    out->max_norm_defect = mx(r.norm);
+    const double m = std::max(std::max(out->max_right_defect, out->max_left_defect),
+                              std::max(out->max_translation_defect, out->max_norm_defect));
+    out->pass = m <= tol ? 1 : 0;
+    out->reserved = 0;
+    for (uint64_t k = 0; k < L; ++k) {
+      if (right_defects) right_defects[k] = r.right[k];
+      if (left_defects) left_defects[k] = r.left[k];
+      if (translation_defects) translation_defects[k] = r.translation[k];
+      if (norm_defects) norm_defects[k] = r.norm[k];
+    }
   });
 }
 

@@ -307,6 +307,107 @@ double right_defect(Engine& e, const double2* b, long long d, long long chi_l, l
   return out;
 }
 
+namespace {
+__global__ void maxabs_diff_partial_kernel(const double2* __restrict__ a, const double2* __restrict__ b, long long n,
+                                           double* part) {
+  __shared__ double sh[256];
+  double m = 0.0;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    m = fmax(m, hypot(a[e].x - b[e].x, a[e].y - b[e].y));
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// max_ij |a_ij - b_ij| (mps.cpp:16-20 on a difference), synchronous
+double maxabs_diff(Engine& e, const double2* a, const double2* b, long long n) {
+  double* part = e.dbuf(S_NORM_PART, 296);
+  maxabs_diff_partial_kernel<<<148, 256, 0, e.stream>>>(a, b, n, part);
+  QT_LAUNCHED();
+  max_final_kernel<<<1, 32, 0, e.stream>>>(part, 148, e.dscal + SC_TMP1);
+  QT_LAUNCHED();
+  double out = 0;
+  QT_CUDA(cudaMemcpyAsync(&out, e.dscal + SC_TMP1, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  return out;
+}
+
+// out = sum_i B^iH mu B^i, B (d, cl, cr): the one-site transfer on mu = conj(lambda)
+// (translate_left_weight, mps.cpp:50-54, conjugated: lambda = Xi^T conj(Xi) = conj(Xi^H Xi))
+void transfer_mu(Engine& e, const double2* mu, const double2* b, long long d, long long cl, long long cr,
+                 double2* tmp, double2* out) {
+  GemmDesc g;  // tmp[i] = mu B^i
+  g.M = cl;
+  g.N = cr;
+  g.K = cl;
+  g.batch = static_cast<int>(d);
+  g.A = mu;
+  g.lda = cl;
+  g.strideA = 0;
+  g.B = b;
+  g.ldb = cr;
+  g.strideB = cl * cr;
+  g.C = tmp;
+  g.ldc = cr;
+  g.strideC = cl * cr;
+  zgemm(g, e.gemm_scratch(), e.stream);
+  gemm(e, Op::H, Op::N, cr, cr, d * cl, b, cr, tmp, cr, out, cr);  // B_stack^H tmp_stack
+}
+}  // namespace
+
+IsometryParts check_isometric_uniform(Engine& e, long long d, const std::vector<long long>& chi,
+                                      const std::vector<const double2*>& sites,
+                                      const std::vector<const double2*>& bonds) {
+  const int L = static_cast<int>(sites.size());
+  IsometryParts r;
+  r.right.resize(L);
+  r.left.resize(L);
+  r.translation.resize(L);
+  r.norm.resize(L);
+  long long cmax = 1;
+  for (long long c : chi) cmax = std::max(cmax, c);
+  // mu_m = Xi_m^H Xi_m for every bond, then the transfer scratch
+  double2* mus = e.cbuf(S_GRAM, static_cast<size_t>(L) * cmax * cmax + 2 * cmax * cmax);
+  double2* cur = mus + static_cast<size_t>(L) * cmax * cmax;
+  double2* nxt = cur + cmax * cmax;
+  double2* tmp = e.cbuf(S_W, d * cmax * cmax);
+  for (int m = 0; m < L; ++m) {
+    const long long c = chi[m];
+    r.right[m] = right_defect(e, sites[m], d, c, chi[(m + 1) % L]);
+    norm2(e, bonds[m], c, c, c, e.dscal + SC_TMP2);
+    double n2 = 0;
+    QT_CUDA(cudaMemcpyAsync(&n2, e.dscal + SC_TMP2, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+    QT_CUDA(cudaStreamSynchronize(e.stream));
+    r.norm[m] = std::abs(std::sqrt(n2) - 1.0);
+    gemm(e, Op::H, Op::N, c, c, c, bonds[m], c, bonds[m], c, mus + static_cast<size_t>(m) * cmax * cmax, c);
+  }
+  for (int m = 0; m < L; ++m) {
+    const int m1 = (m + 1) % L;
+    const long long cl = chi[m], cr = chi[m1];
+    const double2* mu_m = mus + static_cast<size_t>(m) * cmax * cmax;
+    // translation defect: lambda_m T_m vs lambda_{m+1}
+    transfer_mu(e, mu_m, sites[m], d, cl, cr, tmp, nxt);
+    r.translation[m] = maxabs_diff(e, nxt, mus + static_cast<size_t>(m1) * cmax * cmax, cr * cr);
+    // cell fixed point: lambda_m through the L site transfers of the cell
+    copy2d(e, mu_m, cl, cur, cl, cl, cl);
+    long long cc = cl;
+    for (int k = 0; k < L; ++k) {
+      const int s = (m + k) % L;
+      const long long cn = chi[(s + 1) % L];
+      transfer_mu(e, cur, sites[s], d, cc, cn, tmp, nxt);
+      std::swap(cur, nxt);
+      cc = cn;
+    }
+    r.left[m] = maxabs_diff(e, cur, mu_m, cl * cl);
+  }
+  return r;
+}
+
 double bond_energy(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
                    const double2* h) {
   // E = <theta0|h theta0>/<theta0|theta0>, theta0 = Xi Bm Bn

@@ -68,6 +68,16 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
 // pointer (engine slot S_EIG_W) to min(p,q) values
 double* singular_values_device(Engine& e, const double2* m, long long p, long long q);
 
+// check_isometric(UniformMPS), proj/src/mps.cpp:105-141: per-site right
+// defects, per-bond cell fixed-point ("left") and translation defects of the
+// left weights, and per-bond norm defects
+struct IsometryParts {
+  std::vector<double> right, left, translation, norm;
+};
+IsometryParts check_isometric_uniform(Engine& e, long long d, const std::vector<long long>& chi,
+                                      const std::vector<const double2*>& sites,
+                                      const std::vector<const double2*>& bonds);
+
 // device-resident UniformMPS with graph-replayed steps (uniform.cu)
 struct UniformDev;
 UniformDev* uniform_create(Engine& e, int L, long long d, const std::vector<long long>& chi,

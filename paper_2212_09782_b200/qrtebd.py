@@ -355,6 +355,40 @@ def right_defect(b, ctx: Context = None) -> float:
     return out.value
 
 
+@dataclass
+class IsometryReport:
+    """proj/include/qrtebd/mps.hpp:40-53."""
+    right_defects: List[float]
+    left_defects: List[float]
+    translation_defects: List[float]
+    norm_defects: List[float]
+    max_right_defect: float
+    max_left_defect: float
+    max_translation_defect: float
+    max_norm_defect: float
+    passed: bool
+
+    def max_defect(self) -> float:
+        return max(self.max_right_defect, self.max_left_defect, self.max_translation_defect, self.max_norm_defect)
+
+
+def check_isometric(state: UniformMPS, tol: float, ctx: Context = None) -> IsometryReport:
+    """check_isometric(UniformMPS), proj/src/mps.cpp:105-141, on the device."""
+    ctx = ctx or default_context()
+    L = state.cell_length()
+    sites = [_dev(ctx, t) for t in state.site_tensors]
+    bonds = [_dev(ctx, t) for t in state.bond_matrices]
+    sa = (C.c_void_p * L)(*[t.h for t in sites])
+    ba = (C.c_void_p * L)(*[t.h for t in bonds])
+    arrs = [(C.c_double * L)() for _ in range(4)]
+    rep = _capi.qt_isometry_report()
+    check(ctx.lib.qt_check_isometric_uniform(ctx.h, L, C.cast(sa, _capi.PP), C.cast(ba, _capi.PP), tol,
+                                             *arrs, C.byref(rep)))
+    r, l, t, n = ([a[i] for i in range(L)] for a in arrs)
+    return IsometryReport(r, l, t, n, rep.max_right_defect, rep.max_left_defect, rep.max_translation_defect,
+                          rep.max_norm_defect, bool(rep.pass_))
+
+
 def bond_energy(xi, b_m, b_n, h_bond, ctx: Context = None) -> float:
     """Bond energy extension."""
     ctx = ctx or default_context()

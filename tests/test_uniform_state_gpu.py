@@ -103,3 +103,34 @@ def test_concurrent_same_parity_updates_bitwise_equal_serial(ctx, L):
     snap = dev_g.snapshot()
     for s in range(L):
         assert abs(q.expectation_local(snap, z, s, ctx) - ref.expectation_local(st_o, z, s)) < 1e-10
+
+
+@pytest.mark.parametrize("L,chi", [(2, 12), (4, 8)])
+def test_check_isometric_matches_oracle(ctx, L, chi):
+    """check_isometric(UniformMPS), proj/src/mps.cpp:105-141 (IsometryReport,
+    SURVEY.md §8 a12): device defects equal the oracle's to rounding, on a
+    random (non-canonical) cell and on a TEBD-evolved one."""
+    d = 3
+    rng = np.random.default_rng(L * 7 + chi)
+    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(L)]
+    bonds = []
+    for _ in range(L):
+        x = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+        bonds.append(x / np.linalg.norm(x))
+    st_o = ref.UniformMPS(d, sites, bonds)
+    ok_o, mx_o, parts = ref.check_isometric_uniform(st_o, 1e-8)
+    st = q.UniformMPS.from_numpy(ctx, d, sites, bonds)
+    rep = q.check_isometric(st, 1e-8, ctx)
+    for key, dev in (("right", rep.right_defects), ("left", rep.left_defects),
+                     ("translation", rep.translation_defects), ("norm", rep.norm_defects)):
+        np.testing.assert_allclose(dev, parts[key], rtol=1e-10, atol=1e-13)
+    assert rep.passed == ok_o and abs(rep.max_defect() - mx_o) <= 1e-10 * max(mx_o, 1e-3)
+    # after TEBD steps the cell is canonical to rounding: both agree it passes
+    sched = model.trotter_schedule(model.bond_hamiltonian(d, 2.0), 0.05, 2)
+    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0)
+    for _ in range(3):
+        st, _ = q.tebd_step(st, sched, "qr", pol, ctx)
+    rep2 = q.check_isometric(st, 1e-6, ctx)
+    st2 = ref.UniformMPS(d, [t.numpy() for t in st.site_tensors], [b.numpy() for b in st.bond_matrices])
+    ok2, mx2, _ = ref.check_isometric_uniform(st2, 1e-6)
+    assert rep2.passed == ok2 and abs(rep2.max_defect() - mx2) <= 1e-12
