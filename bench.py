@@ -205,6 +205,25 @@ def barrier(ws):
         dist.barrier()
 
 
+def host_info():
+    """CPU model, sockets, cores and NUMA nodes of the host the CPU baseline ran on."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        model, phys = None, set()
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name") and model is None:
+                    model = ln.split(":", 1)[1].strip()
+                elif ln.startswith("physical id"):
+                    phys.add(ln.split(":", 1)[1].strip())
+        info["model"] = model
+        info["sockets"] = len(phys) or None
+        info["numa_nodes"] = len([x for x in os.listdir("/sys/devices/system/node") if x.startswith("node")])
+    except OSError:
+        pass
+    return info
+
+
 def cpu_reference_rate(cfg, budget_s, min_steps=1, warmup=0, seed=0x51AB):
     """Reference algorithm on the host cores: the oracle port (test infra)."""
     from oracle import qrtebd_oracle as ref
@@ -570,7 +589,9 @@ def main():
         rate, n, dt = cpu_reference_rate(cfg, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                                 "sample": f"{n} Trotter steps ({dt:.1f} s) of the NumPy/LAPACK oracle on the same "
-                                          f"config, OpenBLAS threads = {os.cpu_count()}"}
+                                          f"config, OpenBLAS threads = {os.cpu_count()}; LAPACK is likely faster "
+                                          "than the reference's Eigen, so speedups against it are conservative",
+                                "host": host_info()}
         # the reference's SVD-TEBD comparator (gates.cpp:312-322) on the same cell
         # and truncation, timed beside it
         cfg_svd = (cfg[0], cfg[1], cfg[2], "svd", cfg[4], cfg[5])
