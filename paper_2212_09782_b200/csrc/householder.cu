@@ -109,10 +109,26 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_kernel(PanelArgs a) {
     if (blockIdx.x == 0 && w == 1) a.diag[par * NB + k] = P[c * NB + k];
     grid_sync(a.bar, G);
 
-    // ---- phase 2: combine partials (fixed order) and form the reflector
+    // ---- phase 2: combine partials (fixed order) and form the reflector;
+    // warp w sums the CTAs b = w (mod 8) with four independent chains (the
+    // L2 loads of the G partial rows issue in parallel), then warp 0 adds the
+    // eight warp sums in order
+    {
+      double2 s0 = make_double2(0.0, 0.0), s1 = s0, s2 = s0, s3 = s0;
+      unsigned b = w;
+      for (; b + 3 * PANEL_WARPS < G; b += 4 * PANEL_WARPS) {
+        s0 = cadd(s0, __ldcg(&a.part[(size_t(par) * G + b) * NB + k]));
+        s1 = cadd(s1, __ldcg(&a.part[(size_t(par) * G + b + PANEL_WARPS) * NB + k]));
+        s2 = cadd(s2, __ldcg(&a.part[(size_t(par) * G + b + 2 * PANEL_WARPS) * NB + k]));
+        s3 = cadd(s3, __ldcg(&a.part[(size_t(par) * G + b + 3 * PANEL_WARPS) * NB + k]));
+      }
+      for (; b < G; b += PANEL_WARPS) s0 = cadd(s0, __ldcg(&a.part[(size_t(par) * G + b) * NB + k]));
+      red[w * NB + k] = cadd(cadd(s0, s1), cadd(s2, s3));
+    }
+    __syncthreads();
     if (w == 0) {
-      double2 s = make_double2(0.0, 0.0);
-      for (unsigned b = 0; b < G; ++b) s = cadd(s, __ldcg(&a.part[(size_t(par) * G + b) * NB + k]));
+      double2 s = red[k];
+      for (int ww = 1; ww < PANEL_WARPS; ++ww) s = cadd(s, red[ww * NB + k]);
       ssum[k] = s;
     }
     __syncthreads();
