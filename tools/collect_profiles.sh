@@ -20,7 +20,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -s $N0 -c $NP --csv --
 full() {  # name kernel-regex skip command...
   local name=$1 kre=$2 skip=$3; shift 3
   "$@" > $P/plain_$name.log 2>&1 && \
-  ncu --set full --import-source on --clock-control none -k regex:$kre -s $skip -c 1 -o $P/$name "$@" \
+  ncu --set full --import-source on --clock-control none -k "regex:$kre" -s $skip -c 1 -o $P/$name "$@" \
       > $P/ncu_$name.log 2>&1
 }
 full zgemm_c2 zgemm_kernel 1 python tools/gemm_one.py 1280 256 1280 --opb 1 --beta 0
@@ -28,4 +28,7 @@ full zgemm_north zgemm_kernel 1 python tools/gemm_one.py 5120 1024 5120 --opb 1 
 full panel_c2 panel_cluster 8 python tools/qr_one.py 1280 256 2
 full larfb_c2 larfb_cluster 7 python tools/qr_one.py 1280 256 2
 full jacobi_c2cbe jacobi_kernel 1 python tools/eigh_one.py 356
+full larfb32_c2 larfb_cluster 0 python tools/qr_one.py 1280 256 2  # first launch: trailing update, cw = 32
+full permute_c2 permute_kernel 2 python tools/profile_step.py --config c2
+full transpose_c2 transpose_tiled_kernel 1 python tools/profile_step.py --config c2
 tail -1 $P/ncu_*.log
