@@ -23,7 +23,9 @@ def op(x, o):
 
 @pytest.mark.parametrize("opa,opb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("m,n,k", [(64, 128, 16), (37, 53, 29), (5, 7, 3), (200, 130, 300), (1, 1, 1),
-                                   (32, 300, 1000), (25, 64, 25)])
+                                   (32, 300, 1000), (25, 64, 25),
+                                   # makespan-model shapes: split-K over 64 x 128 tiles, K = 32 updates
+                                   (1280, 256, 1280), (2000, 300, 32)])
 def test_zgemm_ops(ctx, opa, opb, m, n, k):
     rng = np.random.default_rng(m * 1000 + n * 10 + k + 7 * opa + 13 * opb)
     a = crand(rng, *((m, k) if opa == 0 else (k, m)))

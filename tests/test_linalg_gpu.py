@@ -22,7 +22,10 @@ def test_qr_known_answer(ctx):
 
 
 @pytest.mark.parametrize("m,n", [(8, 8), (40, 12), (100, 100), (130, 33), (500, 64), (1280, 256), (12, 40),
-                                 (1, 1), (3, 1), (2000, 65)])
+                                 (1, 1), (3, 1), (2000, 65),
+                                 # tall panels: GEMM block reflectors (m > 2048), the register panel at
+                                 # 14/20 rows per warp, and the grid-barrier panel (m > 5120)
+                                 (3000, 40), (5120, 36), (6000, 40)])
 def test_qr_matches_oracle(ctx, m, n):
     rng = np.random.default_rng(m * 31 + n)
     a = crand(rng, m, n)
