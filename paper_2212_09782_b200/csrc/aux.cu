@@ -25,6 +25,16 @@ void Engine::init(int dev, cudaStream_t st) {
   QT_CUDA(cudaMallocHost(&hscal, SC_COUNT * sizeof(double)));
   QT_CUDA(cudaMalloc(&barrier, 64 * sizeof(unsigned)));
   QT_CUDA(cudaMemset(barrier, 0, 64 * sizeof(unsigned)));
+  QT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+}
+
+cudaEvent_t Engine::event(size_t i) {
+  while (events.size() <= i) {
+    cudaEvent_t ev;
+    QT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    events.push_back(ev);
+  }
+  return events[i];
 }
 
 void Engine::destroy() {
@@ -37,6 +47,13 @@ void Engine::destroy() {
   if (dscal) cudaFree(dscal);
   if (hscal) cudaFreeHost(hscal);
   if (barrier) cudaFree(barrier);
+  if (side) {
+    cudaStreamSynchronize(side);
+    cudaStreamDestroy(side);
+  }
+  side = nullptr;
+  for (cudaEvent_t ev : events) cudaEventDestroy(ev);
+  events.clear();
   dscal = nullptr;
   hscal = nullptr;
   barrier = nullptr;

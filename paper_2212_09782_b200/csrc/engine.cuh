@@ -62,6 +62,12 @@ struct Engine {
   double* hscal = nullptr;   // pinned host mirror
   unsigned* barrier = nullptr;  // grid-barrier words (count, generation)
   int num_sms = kNumSMs;
+  // second stream for work that overlaps the main stream inside one call
+  // (the QR trailing update behind the next panel); forks and joins through
+  // events, so it is captured into CUDA graphs with the main stream
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t event(size_t i);
 
   void init(int dev, cudaStream_t st);
   void destroy();

@@ -393,6 +393,12 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   if (dbg_on && !dbg_buf) QT_CUDA(cudaMalloc(&dbg_buf, 8 * NB * sizeof(long long)));
   base.dbg = dbg_on ? dbg_buf : nullptr;
 
+  // look-ahead of the trailing update when every block reflector fits one
+  // cluster (m <= 16 x 128); QT_QR_NO_LOOKAHEAD disables it
+  static const bool la_env = std::getenv("QT_QR_NO_LOOKAHEAD") == nullptr;
+  const bool lookahead = la_env && npan >= 2 && e.side != nullptr && larfb_cluster_fits(m);
+  bool wide_pending = false;
+  long long last_wide = -1;
   for (long long p = 0; p < npan; ++p) {
     const long long j = p * NB;
     const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
@@ -421,6 +427,25 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
       std::fprintf(stderr, "\n");
     }
     const long long ntr = n - j - nbp;
+    if (lookahead && ntr > 0) {
+      // look-ahead: H_p reaches the next panel's columns first (main stream,
+      // after the side stream finished H_{p-1} on them); the rest of the
+      // trailing matrix is updated on the side stream while panel p+1 runs
+      const long long nn = std::min<long long>(NB, ntr);
+      if (p > 0 && wide_pending) QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(2 * (p - 1) + 1), 0));
+      if (ntr > nn) {
+        QT_CUDA(cudaEventRecord(e.event(2 * p), e.stream));  // panel p done: V_p, T_p ready
+        QT_CUDA(cudaStreamWaitEvent(e.side, e.event(2 * p), 0));
+      }
+      larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, nn, nbp, true, e.stream);
+      wide_pending = ntr > nn;
+      if (wide_pending) {
+        larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp + nn, lda, mp, ntr - nn, nbp, true, e.side);
+        QT_CUDA(cudaEventRecord(e.event(2 * p + 1), e.side));
+        last_wide = p;
+      }
+      continue;
+    }
     if (ntr > 0 && !larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, ntr, nbp, true)) {
       GemmDesc g;
       // W = V^H A_trail
@@ -446,6 +471,8 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
       zgemm(g3, gs, e.stream);
     }
   }
+
+  if (last_wide >= 0) QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(2 * last_wide + 1), 0));  // join the side stream
 
   // explicit thin Q = H_0 ... H_{k-1} I[:, :k], block reflectors backward
   set_identity(e, q, m, k, ldq);

@@ -242,8 +242,8 @@ void larfb_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv, cons
 
 // A (mp x ncols, ld lda) <- (I - V T' V^H) A for a panel of nbp <= 32
 // reflectors; returns false when the panel is too tall for one cluster.
-bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T, double2* A, long long lda,
-                   long long mp, long long ncols, int nbp, bool use_th) {
+// largest cluster the block-reflector kernel can run with (16, 8 or 0)
+int larfb_max_cs() {
   static int max_cs = -1;
   if (max_cs < 0) {
     QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -270,6 +270,22 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
       cudaGetLastError();
     }
   }
+  return max_cs;
+}
+
+// the cluster path covers a panel of mp rows
+bool larfb_cluster_fits(long long mp) {
+  static const bool disabled = std::getenv("QT_NO_LARFB_CLUSTER") != nullptr;
+  const int cs = larfb_max_cs();
+  if (disabled || cs == 0) return false;
+  const long long rpc = ceil_div(std::max<long long>(8, ceil_div(mp, cs)), 8) * 8;
+  return rpc <= LB_MAX_RPC;
+}
+
+bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T, double2* A, long long lda,
+                   long long mp, long long ncols, int nbp, bool use_th, cudaStream_t st = nullptr) {
+  if (!st) st = e.stream;
+  const int max_cs = larfb_max_cs();
   static const bool disabled = std::getenv("QT_NO_LARFB_CLUSTER") != nullptr;
   if (disabled || max_cs == 0 || ncols <= 0) return ncols <= 0 && !disabled && max_cs > 0;
   long long rpc = std::max<long long>(8, ceil_div(mp, max_cs));
@@ -289,7 +305,7 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
   cfg.gridDim = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(ceil_div(ncols, cw)));
   cfg.blockDim = dim3(LB_THREADS);
   cfg.dynamicSmemBytes = larfb_cluster_smem(static_cast<int>(rpc), static_cast<int>(cs), cw);
-  cfg.stream = e.stream;
+  cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = static_cast<unsigned>(cs);
@@ -306,8 +322,8 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
   QT_LAUNCHED();
   if (dbg) {  // QT_LARFB_DEBUG=1: phase timings of CTA (0,0) on stderr
     long long h[9];
-    QT_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, e.stream));
-    QT_CUDA(cudaStreamSynchronize(e.stream));
+    QT_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    QT_CUDA(cudaStreamSynchronize(st));
     std::fprintf(stderr,
                  "larfb mp=%lld ncols=%lld cs=%lld rpc=%lld cw=%d cycles: stage %lld csync %lld W %lld rs %lld ag %lld "
                  "W2 %lld upd %lld exit %lld\n",
