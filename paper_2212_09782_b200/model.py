@@ -86,3 +86,13 @@ def z1_local_vector(d: int) -> np.ndarray:
     v = np.zeros(d, dtype=np.complex128)
     v[0] = 1.0
     return v
+
+
+def random_right_isometry(rng, d: int, chi_l: int, chi_r: int) -> np.ndarray:
+    """Random site tensor B (d, chi_l, chi_r) with sum_i B^i B^i^H = 1 (the
+    bench_cell input recipe, proj/src/run.cpp:345-349): orthonormal rows of
+    the (chi_l, d*chi_r) matrix from a Gaussian QR, gauge-fixed."""
+    g = rng.standard_normal((d * chi_r, chi_l)) + 1j * rng.standard_normal((d * chi_r, chi_l))
+    q, r = np.linalg.qr(g)
+    q = q * (np.diag(r) / np.abs(np.diag(r)))
+    return np.ascontiguousarray(q.conj().T.reshape(chi_l, d, chi_r).transpose(1, 0, 2))

@@ -50,9 +50,8 @@ def main():
         out[f"gemm_{'x'.join(map(str, shp))}"] = tf
     for d, chi in [(5, 256), (5, 1024)]:
         rng = np.random.default_rng(1)
-        from oracle import qrtebd_oracle as ref
-        bm = ref.random_right_isometry(rng, d, chi, chi)
-        bn = ref.random_right_isometry(rng, d, chi, chi)
+        bm = model.random_right_isometry(rng, d, chi, chi)
+        bn = model.random_right_isometry(rng, d, chi, chi)
         xi = crand(rng, chi, chi)
         xi /= np.linalg.norm(xi)
         u = model.make_gate(model.bond_hamiltonian(d, 2.0), 0.05)
@@ -67,7 +66,7 @@ def main():
             upd = q.apply_gate_qr(txi, tbm, tbn, tu, pol, ctx, want_left_iso=False)
         ctx.synchronize()
         dt = (time.perf_counter() - t0) / n
-        f = ref.flops_per_update(d, chi, chi, chi, False)
+        f = __import__('bench').flops_per_update(d, chi, chi, chi, False)
         print("update", d, chi, f"{dt*1e3:.2f} ms", f"{f/dt/1e12:.2f} TF", upd.report, flush=True)
         out[f"update_d{d}_chi{chi}_ms"] = dt * 1e3
     print(json.dumps(out))

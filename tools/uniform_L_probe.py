@@ -6,7 +6,6 @@ import time
 import numpy as np
 
 sys.path.insert(0, ".")
-from oracle import qrtebd_oracle as ref  # noqa: E402  (test infra: random isometries)
 from paper_2212_09782_b200._capi import Context  # noqa: E402
 from paper_2212_09782_b200 import model, qrtebd as q  # noqa: E402
 
@@ -17,7 +16,7 @@ gates = [(p, ctx.tensor(g)) for p, g in sched]
 pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0)
 for L in (2, 4, 8):
     rng = np.random.default_rng(L)
-    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(L)]
+    sites = [model.random_right_isometry(rng, d, chi, chi) for _ in range(L)]
     bonds = [np.eye(chi, dtype=complex) / np.sqrt(chi)] * L
     dev = q.DeviceUniformMPS(q.UniformMPS.from_numpy(ctx, d, sites, bonds), ctx)
     for _ in range(3):
