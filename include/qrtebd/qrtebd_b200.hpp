@@ -364,6 +364,127 @@ inline IsometryReport check_isometric(Context& ctx, const UniformMPS& mps, doubl
   return r;
 }
 
+// ---- FiniteMPS (proj/include/qrtebd/mps.hpp:31-38) with reference semantics -------
+struct FiniteMPS {
+  std::size_t phys_dim = 0;
+  std::vector<ComplexTensor> site_tensors;
+  std::size_t center_bond = 0;
+  ComplexTensor center_matrix;
+  std::size_t length() const { return site_tensors.size(); }
+};
+
+/// One FiniteLayer (proj/include/qrtebd/gates.hpp:130-137).
+struct FiniteLayer {
+  BondParity parity = BondParity::even;
+  double dt = 0.0;
+  std::vector<TwoSiteGate> gates;  // one per bond, indexed by left site
+};
+
+struct FiniteStepResult {
+  FiniteMPS state;
+  std::vector<BondReport> reports;
+};
+
+namespace detail {
+// RAII handle of a device-resident chain (qt_finite)
+class DeviceFinite {
+ public:
+  DeviceFinite(Context& ctx, const FiniteMPS& s) {
+    std::vector<DeviceTensor> sites;
+    std::vector<qt_tensor*> sh;
+    for (const ComplexTensor& t : s.site_tensors) {
+      sites.emplace_back(ctx, t);
+      sh.push_back(sites.back().get());
+    }
+    DeviceTensor c(ctx, s.center_matrix);
+    check(qt_finite_create(ctx.get(), sh.size(), sh.data(), s.center_bond, c.get(), &h_));
+  }
+  ~DeviceFinite() {
+    if (h_) qt_finite_destroy(h_);
+  }
+  DeviceFinite(const DeviceFinite&) = delete;
+  DeviceFinite& operator=(const DeviceFinite&) = delete;
+  qt_finite* get() const { return h_; }
+  FiniteMPS host(std::size_t d, std::size_t n) const {
+    FiniteMPS out;
+    out.phys_dim = d;
+    uint64_t c = 0;
+    check(qt_finite_center_bond(h_, &c));
+    out.center_bond = c;
+    for (std::size_t m = 0; m < n; ++m) {
+      qt_tensor* v = nullptr;
+      check(qt_finite_view(h_, 0, m, &v));
+      out.site_tensors.push_back(DeviceTensor(v).host());
+    }
+    qt_tensor* v = nullptr;
+    check(qt_finite_view(h_, 1, 0, &v));
+    out.center_matrix = DeviceTensor(v).host();
+    return out;
+  }
+
+ private:
+  qt_finite* h_ = nullptr;
+};
+}  // namespace detail
+
+/// move_center, proj/src/mps.cpp:226-257 (value semantics, device QR/LQ)
+inline FiniteMPS move_center(Context& ctx, const FiniteMPS& mps, std::size_t new_center) {
+  detail::DeviceFinite f(ctx, mps);
+  check(qt_finite_move_center(f.get(), new_center));
+  return f.host(mps.phys_dim, mps.length());
+}
+
+/// tebd_step(FiniteMPS), proj/src/gates.cpp:542-578
+inline FiniteStepResult tebd_step(Context& ctx, const FiniteMPS& state, const std::vector<FiniteLayer>& layers,
+                                  Scheme scheme, const TruncationPolicy& policy) {
+  const std::size_t n = state.length();
+  detail::DeviceFinite f(ctx, state);
+  std::vector<DeviceTensor> g;
+  std::vector<qt_tensor*> gh;
+  std::vector<int32_t> par;
+  for (const FiniteLayer& l : layers) {
+    if (l.gates.size() + 1 != n) throw ShapeError("layer gate count must equal the bond count");
+    par.push_back(l.parity == BondParity::even ? 0 : 1);
+    for (const TwoSiteGate& u : l.gates) {
+      g.emplace_back(ctx, u.u);
+      gh.push_back(g.back().get());
+    }
+  }
+  std::vector<qt_bond_report> reps(layers.size() * (n / 2 + 1) + 1);
+  uint64_t cnt = reps.size();
+  const qt_policy p = policy.c();
+  check(qt_finite_step(f.get(), layers.size(), par.data(), gh.data(),
+                       scheme == Scheme::qr ? QT_SCHEME_QR : (scheme == Scheme::qr_cbe ? QT_SCHEME_QR_CBE
+                                                                                       : QT_SCHEME_SVD),
+                       &p, reps.data(), &cnt));
+  FiniteStepResult out;
+  out.state = f.host(state.phys_dim, n);
+  for (uint64_t i = 0; i < cnt; ++i) out.reports.push_back({reps[i].bond, from_c(reps[i].report)});
+  return out;
+}
+
+/// expectation_local(FiniteMPS), proj/src/mps.cpp:188-196
+inline cplx expectation_local(Context& ctx, const FiniteMPS& mps, const ComplexTensor& op, std::size_t site) {
+  if (site >= mps.length()) throw InputError("site out of range");
+  const FiniteMPS c = move_center(ctx, mps, site);
+  DeviceTensor xi(ctx, c.center_matrix), b(ctx, c.site_tensors[site]), o(ctx, op);
+  double out[2];
+  check(qt_expectation_local(ctx.get(), xi.get(), b.get(), o.get(), out));
+  return {out[0], out[1]};
+}
+
+/// schmidt_values(FiniteMPS), proj/src/mps.cpp:203-207
+inline std::vector<double> schmidt_values(Context& ctx, const FiniteMPS& mps, std::size_t bond) {
+  if (bond > mps.length()) throw InputError("bond out of range");
+  const FiniteMPS c = move_center(ctx, mps, bond);
+  DeviceTensor xi(ctx, c.center_matrix);
+  std::vector<double> s(std::min(c.center_matrix.dim(0), c.center_matrix.dim(1)));
+  uint64_t cnt = s.size();
+  check(qt_schmidt_values(ctx.get(), xi.get(), s.data(), &cnt));
+  s.resize(cnt);
+  return s;
+}
+
 }  // namespace qrtebd
 
 #endif

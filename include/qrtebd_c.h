@@ -219,6 +219,37 @@ qt_status qt_check_isometric_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tenso
 qt_status qt_bond_energy(qt_ctx* ctx, const qt_tensor* xi, const qt_tensor* b_m, const qt_tensor* b_n,
                          const qt_tensor* h_bond, double* out);
 
+/* ---- finite chain, reference semantics (FiniteMPS, proj/include/qrtebd/mps.hpp:31-38) ----
+ * An open-chain MPS with an explicit orthogonality-center bond kept in HBM:
+ * n site tensors (d, chi_l, chi_r), center_bond in [0, n], and the center
+ * matrix (possibly rectangular after a rank-revealing gauge move,
+ * proj/src/mps.cpp:328-330).  qt_finite_create copies its inputs. */
+typedef struct qt_finite qt_finite;
+qt_status qt_finite_create(qt_ctx* ctx, uint64_t n_sites, qt_tensor* const* sites, uint64_t center_bond,
+                           const qt_tensor* center, qt_finite** out);
+qt_status qt_finite_destroy(qt_finite* f);
+qt_status qt_finite_clone(const qt_finite* f, qt_finite** out);
+qt_status qt_finite_center_bond(const qt_finite* f, uint64_t* out);
+/* which: 0 = site tensor m, 1 = the center matrix (m ignored); non-owning view */
+qt_status qt_finite_view(qt_finite* f, int which, uint64_t m, qt_tensor** out);
+/* move_center, proj/src/mps.cpp:226-257 (in place; QR moves right, LQ moves left) */
+qt_status qt_finite_move_center(qt_finite* f, uint64_t new_center);
+/* tebd_step(FiniteMPS), proj/src/gates.cpp:542-578, in place: layers[l] has
+ * parity parity[l] and one gate per bond, gates[l * (n - 1) + m] acting on
+ * sites (m, m+1) (FiniteLayer, proj/include/qrtebd/gates.hpp:130-137).  The
+ * center is moved onto bond m before every update; QR keeps left_iso and
+ * moves the center to m+1, QR_CBE keeps the center and renormalizes b_m. */
+qt_status qt_finite_step(qt_finite* f, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
+                         qt_scheme scheme, const qt_policy* policy, qt_bond_report* reports, uint64_t* n_reports);
+/* expectation_local(FiniteMPS) (mps.cpp:188-196) on every site and
+ * schmidt_values(FiniteMPS) (mps.cpp:203-207) of every bond 0..n, from one
+ * gauge sweep over a copy of the state.  z_out: 2n doubles or NULL (op NULL
+ * skips them); bond b's values land at schmidt_out[offsets[b] ..
+ * offsets[b+1]) when offsets[n+1] <= cap; offsets (n+2 entries) is always
+ * filled, so a first call with cap = 0 sizes the buffer. */
+qt_status qt_finite_observables(const qt_finite* f, const qt_tensor* op, double* z_out, double* schmidt_out,
+                                uint64_t cap, uint64_t* offsets);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Per-launch CUDA-event profile of the DMMA GEMM kernel (roofline evidence):
  * between begin and end every GEMM launch is bracketed by events; end

@@ -621,6 +621,173 @@ def tebd_step_finite_hastings(sites: List[np.ndarray], bonds: List[np.ndarray], 
     return sites, bonds, reports
 
 
+# --------------------------------------------------------------------- finite (reference semantics)
+@dataclass
+class FiniteMPS:
+    """proj/include/qrtebd/mps.hpp:31-38: sites < center_bond left-isometric,
+    sites >= center_bond right-isometric, center matrix on center_bond."""
+
+    phys_dim: int
+    site_tensors: List[np.ndarray]
+    center_bond: int
+    center_matrix: np.ndarray
+
+    def length(self):
+        return len(self.site_tensors)
+
+    def copy(self):
+        return FiniteMPS(self.phys_dim, [t.copy() for t in self.site_tensors], self.center_bond,
+                         self.center_matrix.copy())
+
+
+def product_state_finite(d: int, n_sites: int, local_vector) -> FiniteMPS:
+    """proj/src/mps.cpp:93-102."""
+    if n_sites == 0:
+        raise InputError("chain length must be positive")
+    v = np.asarray(local_vector, dtype=cplx)
+    if v.shape != (d,):
+        raise ShapeError("local vector length must equal d")
+    n2 = float(np.vdot(v, v).real)
+    if n2 <= 0.0:
+        raise InputError("local vector has zero norm")
+    v = v / math.sqrt(n2)
+    return FiniteMPS(d, [v.reshape(d, 1, 1).copy() for _ in range(n_sites)], 0, np.eye(1, dtype=cplx))
+
+
+def move_center(mps: FiniteMPS, new_center: int) -> FiniteMPS:
+    """proj/src/mps.cpp:226-257 (returns a moved copy)."""
+    if new_center > mps.length():
+        raise InputError("center bond out of range")
+    s = mps.copy()
+    d = s.phys_dim
+    while s.center_bond < new_center:
+        c = s.center_bond
+        m = np.einsum("aq,iqb->aib", s.center_matrix, s.site_tensors[c])  # (a, i, b), mps.cpp:232-233
+        chi_l, chi_r = m.shape[0], m.shape[2]
+        q, r = qr_reduced(m.reshape(chi_l * d, chi_r))
+        k = q.shape[1]
+        s.site_tensors[c] = np.ascontiguousarray(q.reshape(chi_l, d, k).transpose(1, 0, 2))
+        s.center_matrix = r
+        s.center_bond = c + 1
+    while s.center_bond > new_center:
+        c = s.center_bond
+        m = np.einsum("iab,bg->iag", s.site_tensors[c - 1], s.center_matrix)  # (i, a, g), mps.cpp:244-245
+        chi_l, chi_r = m.shape[1], m.shape[2]
+        l, q = lq_reduced(m.transpose(1, 0, 2).reshape(chi_l, d * chi_r))
+        k = q.shape[0]
+        s.site_tensors[c - 1] = np.ascontiguousarray(q.reshape(k, d, chi_r).transpose(1, 0, 2))
+        s.center_matrix = l
+        s.center_bond = c - 1
+    return s
+
+
+def expectation_local_finite(mps: FiniteMPS, op, site: int) -> complex:
+    """proj/src/mps.cpp:188-196."""
+    if op.shape != (mps.phys_dim, mps.phys_dim):
+        raise ShapeError("operator must be d x d")
+    if site >= mps.length():
+        raise InputError("site out of range")
+    c = move_center(mps, site)
+    return expectation_from_weight(left_weight(c.center_matrix), c.site_tensors[site], op)
+
+
+def schmidt_values_finite(mps: FiniteMPS, bond: int):
+    """proj/src/mps.cpp:203-207."""
+    if bond > mps.length():
+        raise InputError("bond out of range")
+    return svd(move_center(mps, bond).center_matrix)[1]
+
+
+def check_isometric_finite(mps: FiniteMPS, tol: float):
+    """proj/src/mps.cpp:143-164; returns (pass, max_defect, parts)."""
+    n = mps.length()
+    right = [0.0] * n
+    left = [0.0] * n
+    for s in range(n):
+        if s < mps.center_bond:
+            left[s] = left_defect(mps.site_tensors[s])
+        else:
+            right[s] = right_defect(mps.site_tensors[s])
+    norm = [abs(np.linalg.norm(mps.center_matrix) - 1.0)]
+    mx = max(max(right), max(left), norm[0])
+    return mx <= tol, mx, dict(right=right, left=left, norm=norm)
+
+
+def finite_layers(d: int, g: float, n_sites: int, dt: float, order: int):
+    """finite_trotter_layers with chain_bond_hamiltonian (proj/include/qrtebd/gates.hpp:160-173,
+    proj/src/clock.cpp:92-99): [(parity, [gate per bond])]."""
+    return [(p, [make_gate(chain_bond_hamiltonian(d, g, b, n_sites), dte) for b in range(n_sites - 1)])
+            for p, dte in layer_structure(dt, order)]
+
+
+def tebd_step_finite(state: FiniteMPS, layers, scheme: str, policy: TruncationPolicy, on_gate=None):
+    """proj/src/gates.cpp:542-578: sequential, center moved onto every bond."""
+    s = state.copy()
+    n_sites = s.length()
+    reports = []
+    for parity, gates in layers:
+        if len(gates) + 1 != n_sites:
+            raise ShapeError("layer gate count must equal the bond count")
+        start = 0 if parity == "even" else 1
+        for m in range(start, n_sites - 1, 2):
+            s = move_center(s, m)
+            upd = apply_gate(scheme, s.center_matrix, s.site_tensors[m], s.site_tensors[m + 1], gates[m], policy)
+            if upd.left_iso is not None:
+                s.site_tensors[m] = upd.left_iso
+                s.center_matrix = upd.xi_n
+                s.center_bond = m + 1
+            else:
+                b_m = upd.b_m
+                eps = upd.report.eps_trunc
+                if not policy.skip_renormalize and 0.0 < eps < 1.0:
+                    b_m = b_m * (1.0 / math.sqrt(1.0 - eps))
+                s.site_tensors[m] = b_m
+            s.site_tensors[m + 1] = upd.b_n
+            reports.append((m + 1, upd.report))
+            if on_gate:
+                on_gate(s, reports[-1])
+    return s, reports
+
+
+# --------------------------------------------------------------------- quench driver
+def run_quench_rows(d: int, g: float, kind: str, size: int, dt: float, t_max: float, order: int, scheme: str,
+                    policy: TruncationPolicy):
+    """run_quench, proj/src/run.cpp:228-326, without the file output: returns
+    one dict per step {t, z[site], entropy[bond], eps[bond], chi[bond],
+    bond_ids, max_eps, max_chi}."""
+    z_op = clock_operators(d)[0]
+    z1 = np.zeros(d, dtype=cplx)
+    z1[0] = 1.0
+    if kind == "uniform":
+        ustate = product_state_uniform(d, size, z1)
+        schedule = trotter_schedule(bond_hamiltonian(d, g, "bulk"), dt, order)
+        bond_ids = list(range(size))
+    else:
+        fstate = product_state_finite(d, size, z1)
+        layers = finite_layers(d, g, size, dt, order)
+        bond_ids = list(range(1, size))
+    n_steps = int(math.floor(t_max / dt + 1e-9))
+    rows = []
+    for k in range(1, n_steps + 1):
+        if kind == "uniform":
+            ustate, reports = tebd_step_uniform(ustate, schedule, scheme, policy)
+            z = [expectation_local(ustate, z_op, s) for s in range(size)]
+            spectra = {b: schmidt_values(ustate, b) for b in bond_ids}
+        else:
+            fstate, reports = tebd_step_finite(fstate, layers, scheme, policy)
+            z = [expectation_local_finite(fstate, z_op, s) for s in range(size)]
+            spectra = {b: schmidt_values_finite(fstate, b) for b in bond_ids}
+        row = dict(t=k * dt, z=z, bond_ids=bond_ids, entropy=[], eps=[], chi=[])
+        for b in bond_ids:
+            row["entropy"].append(entropy_from_schmidt(spectra[b]))
+            row["chi"].append(len(spectra[b]))
+            row["eps"].append(max([0.0] + [r.eps_trunc for bb, r in reports if bb == b]))
+        row["max_eps"] = max([0.0] + [r.eps_trunc for _, r in reports])
+        row["max_chi"] = max(row["chi"])
+        rows.append(row)
+    return rows
+
+
 # --------------------------------------------------------------------- ED helpers
 def two_site_ed_schmidt(u, v, w):
     """proj/tests/test_gates.cc:50-60: Schmidt values of U (v x w)."""

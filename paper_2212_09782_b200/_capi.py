@@ -106,6 +106,15 @@ SIGNATURES = {
     "qt_uniform_step": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int, C.POINTER(qt_policy), C.c_int32,
                                   C.POINTER(qt_bond_report), U64P]),
     "qt_uniform_view": (C.c_int, [P, C.c_int, C.c_uint64, PP]),
+    "qt_finite_create": (C.c_int, [P, C.c_uint64, PP, C.c_uint64, P, PP]),
+    "qt_finite_destroy": (C.c_int, [P]),
+    "qt_finite_clone": (C.c_int, [P, PP]),
+    "qt_finite_center_bond": (C.c_int, [P, U64P]),
+    "qt_finite_view": (C.c_int, [P, C.c_int, C.c_uint64, PP]),
+    "qt_finite_move_center": (C.c_int, [P, C.c_uint64]),
+    "qt_finite_step": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int, C.POINTER(qt_policy),
+                                 C.POINTER(qt_bond_report), U64P]),
+    "qt_finite_observables": (C.c_int, [P, P, DP, DP, C.c_uint64, U64P]),
     "qt_expectation_local": (C.c_int, [P, P, P, P, DP]),
     "qt_schmidt_values": (C.c_int, [P, P, DP, U64P]),
     "qt_right_defect": (C.c_int, [P, P, DP]),

@@ -781,10 +781,11 @@ qt_status qt_expectation_local(qt_ctx* ctx, const qt_tensor* xi_left, const qt_t
     if (op->rank != 2 || op->shape[0] != d || op->shape[1] != d)
       throw qt::Error(qt::Err::shape, "operator must be d x d");
     if (xi_left->shape[1] != b->shape[1]) throw qt::Error(qt::Err::shape, "bond dimensions disagree");
-    // the left weight needs a square-contractible Xi: lambda = Xi^T conj(Xi) is
-    // (chi x chi) over Xi's column index
-    qt::expectation_local(ctx->eng, xi_left->data, static_cast<long long>(xi_left->shape[0]), b->data,
-                          static_cast<long long>(d), static_cast<long long>(b->shape[2]), op->data, out2);
+    // lambda = Xi^T conj(Xi) is (chi x chi) over Xi's column index; Xi may be
+    // rectangular (the reference finite path's center matrix)
+    qt::expectation_local(ctx->eng, xi_left->data, static_cast<long long>(xi_left->shape[0]),
+                          static_cast<long long>(xi_left->shape[1]), b->data, static_cast<long long>(d),
+                          static_cast<long long>(b->shape[2]), op->data, out2);
   });
 }
 
@@ -907,6 +908,374 @@ qt_status qt_fp64_peak(qt_ctx* ctx, int kind, double* tflops) {
     require(ctx && tflops, qt::Err::input, "qt_fp64_peak: null argument");
     *tflops = qt::fp64_peak_tflops(kind, 5, ctx->eng.stream);
   });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- finite chain, reference semantics
+// FiniteMPS (proj/include/qrtebd/mps.hpp:31-38) resident in HBM: site tensors
+// (d, chi_l, chi_r) and the (possibly rectangular) center matrix on
+// center_bond.  move_center (proj/src/mps.cpp:226-257) and the sequential
+// tebd_step(FiniteMPS) (proj/src/gates.cpp:542-578) run on the device, every
+// contraction on the DMMA GEMM, every QR/LQ on the blocked Householder engine.
+struct qt_finite {
+  qt_ctx* ctx = nullptr;
+  uint64_t d = 0;
+  std::vector<qt_tensor*> sites;
+  qt_tensor* center = nullptr;
+  uint64_t center_bond = 0;
+  ~qt_finite() {
+    for (qt_tensor* t : sites) free_tensor(t);
+    free_tensor(center);
+  }
+};
+
+namespace {
+
+// one gauge move to the right, mps.cpp:231-240:
+// M(a,i,b) = sum_q C(a,q) B(i,q,b);  QR of M ((a i) x b);  B <- Q (d,a,k);  C <- R
+void finite_shift_right(qt_finite* f) {
+  qt::Engine& e = f->ctx->eng;
+  const uint64_t c = f->center_bond;
+  qt_tensor* C = f->center;
+  qt_tensor* B = f->sites[c];
+  const long long p = C->shape[0], q = C->shape[1], d = B->shape[0], r = B->shape[2];
+  if (static_cast<long long>(B->shape[1]) != q) throw qt::Error(qt::Err::shape, "center matrix disagrees with site");
+  const long long rows = p * d, k = std::min(rows, r);
+  double2* M = e.cbuf(qt::S_X, rows * r);
+  {
+    qt::GemmDesc g;
+    g.M = p; g.N = r; g.K = q; g.batch = static_cast<int>(d);
+    g.A = C->data; g.lda = q; g.strideA = 0;
+    g.B = B->data; g.ldb = r; g.strideB = q * r;
+    g.C = M; g.ldc = d * r; g.strideC = r;
+    qt::zgemm(g, e.gemm_scratch(), e.stream);
+  }
+  qt_tensor* R = new_tensor(f->ctx, {static_cast<uint64_t>(k), static_cast<uint64_t>(r)});
+  qt_tensor* S = nullptr;
+  try {
+    S = new_tensor(f->ctx, {static_cast<uint64_t>(d), static_cast<uint64_t>(p), static_cast<uint64_t>(k)});
+    double2* Q = e.cbuf(qt::S_QM, rows * k);
+    qt::qr_inplace(e, M, rows, r, r, Q, k, R->data, r);
+    const long long shp[3] = {p, d, k};
+    const int perm[3] = {1, 0, 2};
+    qt::permute(e, Q, 3, shp, perm, false, S->data);  // (a,i,k) -> (i,a,k), mps.cpp:237-238
+  } catch (...) {
+    free_tensor(R);
+    free_tensor(S);
+    throw;
+  }
+  free_tensor(B);
+  free_tensor(C);
+  f->sites[c] = S;
+  f->center = R;
+  f->center_bond = c + 1;
+}
+
+// one gauge move to the left, mps.cpp:242-254:
+// M(i,a,g) = sum_b B(i,a,b) C(b,g);  LQ of M as a x (i g);  B <- Q (d,k,g);  C <- L.
+// LQ(m) = QR(m^H)^H (linalg.cpp:53-64): m^H[(i g), a] = (C^H B[i]^H)[g, a] is formed
+// directly by the batched GEMM, so no transpose of M is materialized.
+void finite_shift_left(qt_finite* f) {
+  qt::Engine& e = f->ctx->eng;
+  const uint64_t c = f->center_bond;
+  qt_tensor* C = f->center;
+  qt_tensor* B = f->sites[c - 1];
+  const long long d = B->shape[0], a = B->shape[1], b = B->shape[2], gdim = C->shape[1];
+  if (static_cast<long long>(C->shape[0]) != b) throw qt::Error(qt::Err::shape, "center matrix disagrees with site");
+  const long long rows = d * gdim, k = std::min(rows, a);
+  double2* MH = e.cbuf(qt::S_X, rows * a);
+  {
+    qt::GemmDesc g;
+    g.M = gdim; g.N = a; g.K = b; g.batch = static_cast<int>(d);
+    g.opA = qt::Op::H; g.A = C->data; g.lda = gdim; g.strideA = 0;
+    g.opB = qt::Op::H; g.B = B->data; g.ldb = b; g.strideB = a * b;
+    g.C = MH; g.ldc = a; g.strideC = gdim * a;
+    qt::zgemm(g, e.gemm_scratch(), e.stream);
+  }
+  qt_tensor* Lt = new_tensor(f->ctx, {static_cast<uint64_t>(a), static_cast<uint64_t>(k)});
+  qt_tensor* S = nullptr;
+  try {
+    S = new_tensor(f->ctx, {static_cast<uint64_t>(d), static_cast<uint64_t>(k), static_cast<uint64_t>(gdim)});
+    double2* Qh = e.cbuf(qt::S_QM, rows * k);
+    double2* Rh = e.cbuf(qt::S_RM, k * a);
+    qt::qr_inplace(e, MH, rows, a, a, Qh, k, Rh, a);
+    const long long s1[2] = {k, a};
+    const int t2[2] = {1, 0};
+    qt::permute(e, Rh, 2, s1, t2, true, Lt->data);  // L = Rh^H (a x k)
+    // site[i,kk,g] = Q[kk,(i g)] = conj(Qh[(i g),kk])   (mps.cpp:251-252)
+    const long long s3[3] = {d, gdim, k};
+    const int p3[3] = {0, 2, 1};
+    qt::permute(e, Qh, 3, s3, p3, true, S->data);
+  } catch (...) {
+    free_tensor(Lt);
+    free_tensor(S);
+    throw;
+  }
+  free_tensor(B);
+  free_tensor(C);
+  f->sites[c - 1] = S;
+  f->center = Lt;
+  f->center_bond = c - 1;
+}
+
+void finite_move_center(qt_finite* f, uint64_t target) {
+  if (target > f->sites.size()) throw qt::Error(qt::Err::input, "center bond out of range");
+  while (f->center_bond < target) finite_shift_right(f);
+  while (f->center_bond > target) finite_shift_left(f);
+}
+
+qt_tensor* clone_tensor(qt_ctx* ctx, const qt_tensor* src) {
+  qt_tensor* t = src->rank == 3 ? new_tensor(ctx, {src->shape[0], src->shape[1], src->shape[2]})
+                                : new_tensor(ctx, {src->shape[0], src->shape[1]});
+  QT_CUDA(cudaMemcpyAsync(t->data, src->data, src->numel() * sizeof(double2), cudaMemcpyDeviceToDevice,
+                          ctx->eng.stream));
+  return t;
+}
+
+}  // namespace
+
+extern "C" {
+
+qt_status qt_finite_create(qt_ctx* ctx, uint64_t n_sites, qt_tensor* const* sites, uint64_t center_bond,
+                           const qt_tensor* center, qt_finite** out) {
+  return guard([&] {
+    require(ctx && sites && center && out, qt::Err::input, "qt_finite_create: null argument");
+    if (n_sites == 0) throw qt::Error(qt::Err::input, "chain length must be positive");
+    if (center_bond > n_sites) throw qt::Error(qt::Err::input, "center bond out of range");
+    require_tensor(center, 2, "finite center matrix");
+    const uint64_t d = sites[0] ? sites[0]->shape[0] : 0;
+    for (uint64_t m = 0; m < n_sites; ++m) {
+      require_tensor(sites[m], 3, "finite site");
+      if (sites[m]->shape[0] != d) throw qt::Error(qt::Err::shape, "physical dimensions disagree");
+      if (m + 1 < n_sites && sites[m]->shape[2] != sites[m + 1]->shape[1])
+        throw qt::Error(qt::Err::shape, "bond dimensions disagree");
+    }
+    auto* f = new qt_finite;
+    f->ctx = ctx;
+    f->d = d;
+    f->center_bond = center_bond;
+    try {
+      for (uint64_t m = 0; m < n_sites; ++m) f->sites.push_back(clone_tensor(ctx, sites[m]));
+      f->center = clone_tensor(ctx, center);
+    } catch (...) {
+      delete f;
+      throw;
+    }
+    *out = f;
+  });
+}
+
+qt_status qt_finite_destroy(qt_finite* f) {
+  return guard([&] { delete f; });
+}
+
+qt_status qt_finite_clone(const qt_finite* f, qt_finite** out) {
+  return guard([&] {
+    require(f && out, qt::Err::input, "qt_finite_clone: null argument");
+    auto* g = new qt_finite;
+    g->ctx = f->ctx;
+    g->d = f->d;
+    g->center_bond = f->center_bond;
+    try {
+      for (const qt_tensor* t : f->sites) g->sites.push_back(clone_tensor(f->ctx, t));
+      g->center = clone_tensor(f->ctx, f->center);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+qt_status qt_finite_center_bond(const qt_finite* f, uint64_t* out) {
+  return guard([&] {
+    require(f && out, qt::Err::input, "qt_finite_center_bond: null argument");
+    *out = f->center_bond;
+  });
+}
+
+qt_status qt_finite_view(qt_finite* f, int which, uint64_t m, qt_tensor** out) {
+  return guard([&] {
+    require(f && out && (which == 0 || which == 1), qt::Err::input, "qt_finite_view: bad argument");
+    if (which == 0 && m >= f->sites.size()) throw qt::Error(qt::Err::input, "site out of range");
+    const qt_tensor* src = which == 0 ? f->sites[m] : f->center;
+    auto* t = new qt_tensor;
+    *t = *src;
+    t->owning = false;
+    *out = t;
+  });
+}
+
+qt_status qt_finite_move_center(qt_finite* f, uint64_t new_center) {
+  return guard([&] {
+    require(f != nullptr, qt::Err::input, "qt_finite_move_center: null argument");
+    finite_move_center(f, new_center);
+  });
+}
+
+qt_status qt_finite_step(qt_finite* f, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
+                         qt_scheme scheme, const qt_policy* policy, qt_bond_report* reports, uint64_t* n_reports) {
+  return guard([&] {
+    require(f && (n_layers == 0 || (parity && gates)), qt::Err::input, "qt_finite_step: null argument");
+    if (scheme != QT_SCHEME_QR && scheme != QT_SCHEME_QR_CBE)
+      throw qt::Error(qt::Err::input, "scheme not available on the device");
+    const qt_policy pol = policy_or_default(policy);
+    qt_ctx* ctx = f->ctx;
+    qt::Engine& e = ctx->eng;
+    const uint64_t n = f->sites.size();
+    const uint64_t nb = n > 0 ? n - 1 : 0;
+    const uint64_t cap = n_reports ? *n_reports : 0;
+    std::vector<qt_bond_report> out;
+    struct Pending {
+      uint64_t bond, before, eta;
+    };
+    std::vector<Pending> pend;  // QR reports whose scalars are still on the device
+    constexpr int kRep = 8;  // dscal[0..7]: theta2, L2, resid, tmp0..tmp3 (the finiteness flag is SC_TMP3)
+    double* rep_dev = e.dbuf(qt::S_REPORTS, kRep * (n_layers * (nb / 2 + 1) + 1));
+    auto flush_qr = [&] {
+      if (pend.empty()) return;
+      std::vector<double> h(kRep * pend.size());
+      QT_CUDA(cudaMemcpyAsync(h.data(), rep_dev, h.size() * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+      QT_CUDA(cudaStreamSynchronize(e.stream));
+      for (size_t i = 0; i < pend.size(); ++i) {
+        qt::HostReport hr;
+        hr.theta2 = h[kRep * i + qt::SC_THETA2];
+        hr.kept2 = h[kRep * i + qt::SC_L2];
+        hr.resid = h[kRep * i + qt::SC_RESID];
+        int flag = 0;
+        std::memcpy(&flag, &h[kRep * i + qt::SC_TMP3], sizeof(int));
+        if (flag) throw qt::Error(qt::Err::input, "qr_reduced: non-finite entries");
+        double eps = 0, disc = 0;
+        report_from(hr, pol, &eps, &disc);
+        qt_bond_report br;
+        br.bond = pend[i].bond;
+        fill_report(&br.report, pend[i].before, pend[i].eta, pend[i].eta, eps, disc, QT_SCHEME_QR);
+        out.push_back(br);
+      }
+      pend.clear();
+    };
+    for (uint64_t l = 0; l < n_layers; ++l) {
+      const uint64_t start = parity[l] == 0 ? 0 : 1;
+      for (uint64_t m = start; m + 1 < n; m += 2) {
+        const qt_tensor* u = gates[l * nb + m];
+        finite_move_center(f, m);  // gates.cpp:556
+        const qt::Dims D = gate_dims(f->center, f->sites[m], f->sites[m + 1], u);
+        if (scheme == QT_SCHEME_QR) {
+          // left_iso present: the center moves onto bond m+1 (gates.cpp:559-563)
+          const long long eta = qt::qr_eta(pol, D);
+          const uint64_t d = D.d;
+          qt_tensor* xi = new_tensor(ctx, {static_cast<uint64_t>(eta), static_cast<uint64_t>(eta)});
+          qt_tensor *bn = nullptr, *left = nullptr;
+          try {
+            bn = new_tensor(ctx, {d, static_cast<uint64_t>(eta), static_cast<uint64_t>(D.chi_r)});
+            left = new_tensor(ctx, {d, static_cast<uint64_t>(D.chi_l), static_cast<uint64_t>(eta)});
+            qt::GateBuffers gb{nullptr, xi->data, bn->data, left->data};
+            qt::gate_qr_async(e, D, f->center->data, f->sites[m]->data, f->sites[m + 1]->data, u->data, pol, eta,
+                              gb);
+          } catch (...) {
+            free_tensor(xi);
+            free_tensor(bn);
+            free_tensor(left);
+            throw;
+          }
+          QT_CUDA(cudaMemcpyAsync(rep_dev + kRep * pend.size(), e.dscal, kRep * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  e.stream));
+          pend.push_back({m + 1, static_cast<uint64_t>(D.chi_n), static_cast<uint64_t>(eta)});
+          free_tensor(f->sites[m]);
+          free_tensor(f->sites[m + 1]);
+          free_tensor(f->center);
+          f->sites[m] = left;
+          f->sites[m + 1] = bn;
+          f->center = xi;
+          f->center_bond = m + 1;
+        } else {
+          // Hastings-only scheme: the center matrix stays put; b_m is renormalized
+          // by 1/sqrt(1 - eps) unless skip_renormalize (gates.cpp:564-571)
+          flush_qr();
+          QrOut o;
+          qt::CbeResult res;
+          try {
+            res = qt::gate_cbe(e, D, f->center->data, f->sites[m]->data, f->sites[m + 1]->data, u->data, pol,
+                               [&](long long kk) {
+                                 const uint64_t k = static_cast<uint64_t>(kk), d = D.d;
+                                 o.b_m = new_tensor(ctx, {d, static_cast<uint64_t>(D.chi_m), k});
+                                 o.xi = new_tensor(ctx, {k, k});
+                                 o.b_n = new_tensor(ctx, {d, k, static_cast<uint64_t>(D.chi_r)});
+                                 return qt::GateBuffers{o.b_m->data, o.xi->data, o.b_n->data, nullptr};
+                               });
+          } catch (...) {
+            o.release();
+            throw;
+          }
+          double eps = 0, disc = 0;
+          report_from(res.rep, pol, &eps, &disc);
+          if (!pol.skip_renormalize && eps > 0.0 && eps < 1.0) {
+            qt_tensor* scaled = clone_tensor(ctx, o.b_m);
+            const long long cnt = static_cast<long long>(o.b_m->numel());
+            const int idp[1] = {0};
+            qt::permute(e, o.b_m->data, 1, &cnt, idp, false, scaled->data, 1.0 / std::sqrt(1.0 - eps));
+            free_tensor(o.b_m);
+            o.b_m = scaled;
+          }
+          qt_bond_report br;
+          br.bond = m + 1;
+          fill_report(&br.report, D.chi_n, res.eta, res.kk, eps, disc, QT_SCHEME_QR_CBE);
+          out.push_back(br);
+          free_tensor(f->sites[m]);
+          free_tensor(f->sites[m + 1]);
+          free_tensor(o.xi);
+          o.xi = nullptr;
+          f->sites[m] = o.b_m;
+          f->sites[m + 1] = o.b_n;
+        }
+      }
+    }
+    flush_qr();
+    for (size_t i = 0; i < out.size() && i < cap; ++i) reports[i] = out[i];
+    if (n_reports) *n_reports = out.size();
+  });
+}
+
+/* Observables of a FiniteMPS in one left-to-right gauge sweep over a copy of
+ * the state: <op> on every site (expectation_local(FiniteMPS), mps.cpp:188-196)
+ * and the Schmidt values of every bond 0..n (schmidt_values(FiniteMPS),
+ * mps.cpp:203-207).  z_out: 2n doubles (re, im) or NULL; schmidt_out: values of
+ * bond b at offsets[b] (offsets has n+2 entries; the values are written only
+ * when the capacity cap suffices, the offsets always). */
+qt_status qt_finite_observables(const qt_finite* f, const qt_tensor* op, double* z_out, double* schmidt_out,
+                                uint64_t cap, uint64_t* offsets) {
+  qt_finite* w = nullptr;
+  qt_status st = guard([&] {
+    require(f != nullptr, qt::Err::input, "qt_finite_observables: null argument");
+    if (op && (op->rank != 2 || op->shape[0] != f->d || op->shape[1] != f->d))
+      throw qt::Error(qt::Err::shape, "operator must be d x d");
+    qt_status cs = qt_finite_clone(f, &w);
+    if (cs != QT_OK) throw qt::Error(qt::Err::internal, qt_last_error());
+    qt::Engine& e = w->ctx->eng;
+    const uint64_t n = w->sites.size();
+    finite_move_center(w, 0);
+    uint64_t off = 0;
+    for (uint64_t b = 0; b <= n; ++b) {
+      if (b > 0) finite_shift_right(w);
+      const long long p = w->center->shape[0], q = w->center->shape[1], k = std::min(p, q);
+      if (offsets) offsets[b] = off;
+      if (schmidt_out && off + k <= cap) {
+        const double* s = qt::singular_values_device(e, w->center->data, p, q);
+        QT_CUDA(cudaMemcpyAsync(schmidt_out + off, s, k * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+        QT_CUDA(cudaStreamSynchronize(e.stream));
+      }
+      off += k;
+      if (b < n && op && z_out) {
+        const qt_tensor* B = w->sites[b];
+        qt::expectation_local(e, w->center->data, p, q, B->data, static_cast<long long>(f->d),
+                              static_cast<long long>(B->shape[2]), op->data, z_out + 2 * b);
+      }
+    }
+    if (offsets) offsets[n + 1] = off;
+  });
+  delete w;
+  return st;
 }
 
 }  // extern "C"

@@ -222,9 +222,11 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     const int perm[3] = {0, 2, 1};
     permute(e, Qp, 3, shp, perm, true, out.b_n);
   }
-  {
+  if (out.b_m) {
     // B~m[i,beta,k] = sum_{j,delta} phiev[beta,i,j,delta] conj(B~n[j,k,delta])
     //             = (phiev (cm*d x d*cr) . Qp)[(beta i), k]   (gates.cpp:186-190)
+    // (skipped when the caller keeps left_iso instead: the reference finite
+    // step discards b_m for QR, gates.cpp:559-563)
     GemmDesc g;
     g.M = cm * d; g.N = eta; g.K = cols;
     g.A = phiev; g.lda = cols;
@@ -266,15 +268,16 @@ HostReport read_report(Engine& e) {
 }
 
 // ------------------------------------------------------------ observables
-void expectation_local(Engine& e, const double2* xi, long long chi_l, const double2* b, long long d,
-                       long long chi_r, const double2* op, double* out2_host) {
-  // M = Xi^H Xi ; lambda = conj(M) (mps.cpp:44-46)
+void expectation_local(Engine& e, const double2* xi, long long xi_rows, long long chi_l, const double2* b,
+                       long long d, long long chi_r, const double2* op, double* out2_host) {
+  // M = Xi^H Xi (Xi is xi_rows x chi_l; rectangular on the reference finite
+  // path, mps.cpp:232-238) ; lambda = conj(M) (mps.cpp:44-46)
   // t1[i] = M^H . B[i]  (= sum_a lambda[a,a'] B[i,a,b], mps.cpp:171)
   // t2 = t1 (d x chi_l*chi_r) . B^H  (mps.cpp:172) ; <O> = tr(op t2^T)
   double2* M = e.cbuf(S_MISC, chi_l * chi_l + d * d + 8);
   double2* t2 = M + chi_l * chi_l;
   double2* t1 = e.cbuf(S_MISC2, d * chi_l * chi_r);
-  gemm(e, Op::H, Op::N, chi_l, chi_l, chi_l, xi, chi_l, xi, chi_l, M, chi_l);
+  gemm(e, Op::H, Op::N, chi_l, chi_l, xi_rows, xi, chi_l, xi, chi_l, M, chi_l);
   {
     GemmDesc g;
     g.M = chi_l; g.N = chi_r; g.K = chi_l; g.batch = static_cast<int>(d);

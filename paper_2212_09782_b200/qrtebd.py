@@ -23,7 +23,8 @@ __all__ = [
     "apply_gate_qr_cbe", "apply_gate", "truncation_error_explicit", "qr_reduced", "lq_reduced", "UniformMPS",
     "product_state_uniform", "tebd_step", "expectation_local", "schmidt_values", "entropy_from_schmidt",
     "entanglement_entropy", "right_defect", "bond_energy", "ShapeError", "InputError", "NumericError",
-    "CapacityError", "QrtebdError", "zgemm",
+    "CapacityError", "QrtebdError", "zgemm", "FiniteMPS", "product_state_finite", "move_center",
+    "tebd_step_finite", "finite_observables",
 ]
 
 _SCHEME_NAMES = {0: "svd", 1: "eig", 2: "qr", 3: "qr_cbe"}
@@ -407,3 +408,159 @@ def eigh(h, ctx: Context = None):
     v = C.c_void_p()
     check(ctx.lib.qt_eigh(ctx.h, t.h, w, C.byref(v)))
     return np.array(w[:n]), DeviceTensor(ctx, v)
+
+
+# --------------------------------------------------------------------- FiniteMPS (reference semantics)
+class FiniteMPS:
+    """FiniteMPS, proj/include/qrtebd/mps.hpp:31-38, resident in HBM (qt_finite).
+
+    Site tensors (d, chi_l, chi_r), an orthogonality-center bond and its
+    (possibly rectangular) center matrix.  move_center and tebd_step run in
+    place on the device; snapshot()/to_numpy() fetch the state."""
+
+    def __init__(self, phys_dim: int, site_tensors, center_bond: int, center_matrix, ctx: Context = None):
+        self.ctx = ctx or default_context()
+        sites = [_dev(self.ctx, t) for t in site_tensors]
+        cm = _dev(self.ctx, center_matrix)
+        n = len(sites)
+        arr = (C.c_void_p * max(1, n))(*[t.h for t in sites])
+        h = C.c_void_p()
+        check(self.ctx.lib.qt_finite_create(self.ctx.h, n, arr, center_bond, cm.h, C.byref(h)))
+        self.h = h
+        self.phys_dim = phys_dim
+        self.n = n
+
+    @classmethod
+    def _adopt(cls, ctx: Context, handle, phys_dim: int, n: int) -> "FiniteMPS":
+        obj = cls.__new__(cls)
+        obj.ctx, obj.h, obj.phys_dim, obj.n = ctx, handle, phys_dim, n
+        return obj
+
+    def close(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.qt_finite_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def length(self) -> int:
+        return self.n
+
+    @property
+    def center_bond(self) -> int:
+        out = C.c_uint64()
+        check(self.ctx.lib.qt_finite_center_bond(self.h, C.byref(out)))
+        return int(out.value)
+
+    def view(self, which: str, m: int = 0) -> DeviceTensor:
+        """Non-owning view of site tensor m ('site') or of the center matrix ('center')."""
+        h = C.c_void_p()
+        check(self.ctx.lib.qt_finite_view(self.h, 0 if which == "site" else 1, m, C.byref(h)))
+        return DeviceTensor(self.ctx, h)
+
+    @property
+    def center_matrix(self) -> np.ndarray:
+        return self.view("center").numpy()
+
+    def site(self, m: int) -> np.ndarray:
+        return self.view("site", m).numpy()
+
+    def copy(self) -> "FiniteMPS":
+        h = C.c_void_p()
+        check(self.ctx.lib.qt_finite_clone(self.h, C.byref(h)))
+        return FiniteMPS._adopt(self.ctx, h, self.phys_dim, self.n)
+
+    def to_numpy(self):
+        """(site tensors, center_bond, center matrix) as NumPy arrays."""
+        return [self.site(m) for m in range(self.n)], self.center_bond, self.center_matrix
+
+
+def product_state_finite(d: int, n_sites: int, local_vector, ctx: Context = None) -> FiniteMPS:
+    """proj/src/mps.cpp:93-102."""
+    if n_sites == 0:
+        raise InputError("chain length must be positive")
+    v = np.asarray(local_vector, dtype=np.complex128)
+    if v.shape != (d,):
+        raise ShapeError("local vector length must equal d")
+    n2 = float(np.vdot(v, v).real)
+    if n2 <= 0:
+        raise InputError("local vector has zero norm")
+    v = v / math.sqrt(n2)
+    return FiniteMPS(d, [v.reshape(d, 1, 1)] * n_sites, 0, np.eye(1, dtype=np.complex128), ctx)
+
+
+def move_center(state: FiniteMPS, new_center: int) -> FiniteMPS:
+    """move_center, proj/src/mps.cpp:226-257: value semantics (a moved copy)."""
+    out = state.copy()
+    check(out.ctx.lib.qt_finite_move_center(out.h, new_center))
+    return out
+
+
+def tebd_step_finite(state: FiniteMPS, layers, scheme: str, policy=None, in_place: bool = False):
+    """tebd_step(FiniteMPS), proj/src/gates.cpp:542-578 (reference semantics:
+    the center is moved onto every bond before its gate).
+
+    layers: [(parity 'even'|'odd', [gate per bond m, acting on (m, m+1)])]
+    (FiniteLayer, proj/include/qrtebd/gates.hpp:130-137).  Returns
+    (new FiniteMPS, [BondReport]); in_place=True updates `state` itself."""
+    s = state if in_place else state.copy()
+    ctx = s.ctx
+    nb = s.n - 1
+    flat = []
+    for _, gates in layers:
+        if len(gates) != nb:
+            raise ShapeError("layer gate count must equal the bond count")
+        flat.extend(_dev(ctx, g) for g in gates)
+    s._gates = flat
+    par = (C.c_int32 * max(1, len(layers)))(*[0 if p == "even" else 1 for p, _ in layers])
+    gh = (C.c_void_p * max(1, len(flat)))(*[g.h for g in flat])
+    cap = len(layers) * (nb // 2 + 1)
+    reps = (qt_bond_report * max(1, cap))()
+    n = C.c_uint64(cap)
+    pol = _policy(policy)
+    check(ctx.lib.qt_finite_step(s.h, len(layers), par, gh, _capi.SCHEME_IDS[scheme], C.byref(pol), reps,
+                                 C.byref(n)))
+    out = [BondReport(int(reps[i].bond), TruncationReport.from_c(reps[i].report)) for i in range(n.value)]
+    return s, out
+
+
+def finite_observables(state: FiniteMPS, op=None):
+    """<op> on every site (expectation_local(FiniteMPS), mps.cpp:188-196) and
+    the Schmidt values of every bond 0..n (schmidt_values(FiniteMPS),
+    mps.cpp:203-207), from one device gauge sweep: returns (z, [spectra])."""
+    ctx = state.ctx
+    n = state.n
+    top = _dev(ctx, op) if op is not None else None
+    offs = (C.c_uint64 * (n + 2))()
+    z = (C.c_double * max(1, 2 * n))()
+    check(ctx.lib.qt_finite_observables(state.h, top.h if top else None, z, None, 0, offs))
+    total = int(offs[n + 1])
+    buf = (C.c_double * max(1, total))()
+    check(ctx.lib.qt_finite_observables(state.h, None, None, buf, total, offs))
+    zs = np.array([complex(z[2 * s], z[2 * s + 1]) for s in range(n)]) if top is not None else None
+    spectra = [np.array(buf[int(offs[b]):int(offs[b + 1])]) for b in range(n + 1)]
+    return zs, spectra
+
+
+def expectation_local_finite(state: FiniteMPS, op, site: int) -> complex:
+    """expectation_local(FiniteMPS), proj/src/mps.cpp:188-196."""
+    if site >= state.n:
+        raise InputError("site out of range")
+    c = move_center(state, site)
+    out = (C.c_double * 2)()
+    top = _dev(c.ctx, op)
+    cv, sv = c.view("center"), c.view("site", site)  # keep the view handles alive across the call
+    check(c.ctx.lib.qt_expectation_local(c.ctx.h, cv.h, sv.h, top.h, out))
+    return complex(out[0], out[1])
+
+
+def schmidt_values_finite(state: FiniteMPS, bond: int) -> np.ndarray:
+    """schmidt_values(FiniteMPS), proj/src/mps.cpp:203-207."""
+    if bond > state.n:
+        raise InputError("bond out of range")
+    c = move_center(state, bond)
+    return schmidt_values_of(c.view("center"), c.ctx)

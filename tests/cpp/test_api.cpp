@@ -79,6 +79,30 @@ int main() {
   if (r.reports.size() != 2) ++fails;
   const double s0 = entanglement_entropy(ctx, r.state, 0);
   if (!(s0 >= 0.0)) ++fails;
+  // finite chain with the reference's sequential semantics (gates.cpp:542-578):
+  // a product state under the identity gate stays put; the center moves to bond 1
+  {
+    FiniteMPS f;
+    f.phys_dim = d;
+    ComplexTensor v({d, 1, 1});
+    v.data()[0] = 1.0;
+    f.site_tensors = {v, v, v};
+    f.center_bond = 0;
+    f.center_matrix = ComplexTensor::identity(1);
+    FiniteLayer lay;
+    lay.parity = BondParity::even;
+    lay.gates = {id, id};
+    const FiniteStepResult fr = tebd_step(ctx, f, {lay}, Scheme::qr, p);
+    if (fr.reports.size() != 1 || fr.state.center_bond != 1) ++fails;
+    ComplexTensor z({d, d});
+    z.data()[0] = 1.0;
+    z.data()[3] = -1.0;
+    for (std::size_t site = 0; site < 3; ++site)
+      if (std::abs(expectation_local(ctx, fr.state, z, site) - cplx(1.0)) > 1e-12) ++fails;
+    const std::vector<double> sv = schmidt_values(ctx, fr.state, 2);
+    if (sv.empty() || std::abs(sv[0] - 1.0) > 1e-12) ++fails;
+    if (move_center(ctx, fr.state, 0).center_bond != 0) ++fails;
+  }
   std::printf("%s: eps=%.3e defect=%.3e S=%.6f\n", fails ? "FAIL" : "OK", upd.report.eps_trunc, defect, s0);
   return fails ? 1 : 0;
 }

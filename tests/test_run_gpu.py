@@ -1,0 +1,84 @@
+"""Quench driver on the device (paper_2212_09782_b200.run): rows against the
+oracle's run_quench (proj/src/run.cpp:228-326) on the same config, the CSV
+file contract and bitwise determinism (proj/tests/test_run.cc:110-137), and
+checkpoints that load back into the device state."""
+import numpy as np
+import pytest
+
+from oracle import qrtebd_oracle as ref
+from paper_2212_09782_b200 import qrtebd as q
+from paper_2212_09782_b200 import run
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare_rows(rows, orows, tol=1e-10, exact_chi=True):
+    assert len(rows) == len(orows)
+    for r, o in zip(rows, orows):
+        assert r.t == o["t"] and r.bond_ids == o["bond_ids"]
+        if exact_chi:
+            assert r.chi == o["chi"] and r.max_chi == o["max_chi"]
+        if o["max_eps"] > 1e-10:
+            break  # Appendix B(2): assert inside the window where truncation is negligible
+        for a, b in zip(r.z, o["z"]):
+            assert abs(a - b) < tol
+        for a, b in zip(r.entropy, o["entropy"]):
+            assert abs(a - b) < tol
+        for a, b in zip(r.eps, o["eps"]):
+            assert abs(a - b) <= 1e-10 * b + 2e-13 * b ** 0.5 + 1e-20  # trajectory floor
+
+
+@pytest.mark.parametrize("kind,size,scheme,d", [("uniform", 2, "qr", 3), ("uniform", 2, "qr_cbe", 3),
+                                                ("uniform", 4, "qr", 2), ("finite", 6, "qr", 2),
+                                                ("finite", 5, "qr_cbe", 3)])
+def test_quench_rows_match_oracle(ctx, kind, size, scheme, d):
+    c = run.RunConfig(d=d, g=2.0, system_kind=kind, system_size=size, dt=0.05, t_max=0.4, scheme=scheme,
+                      chi_max=32)
+    res = run.run_quench(c, ctx)
+    orows = ref.run_quench_rows(d, 2.0, kind, size, 0.05, 0.4, 2, scheme, ref.TruncationPolicy(chi_max=32))
+    # qr_cbe: while the true Schmidt rank is below eta (the first steps from the
+    # product state) the Gram eigenvalues of the null directions are rounding noise
+    # (|w| ~ u ||G||, either sign), so whether s = sqrt(max(w, 0)) ~ 1e-8 passes the
+    # 1e-14 cutoff is noise in the reference as well (Appendix B(iv)); the kept
+    # count is then not a parity quantity, the observables are
+    _compare_rows(res.rows, orows, exact_chi=(scheme == "qr"))
+
+
+def test_quench_deterministic_csv_bodies(ctx, tmp_path):
+    # test_run.cc:110-137 on the device: identical configs -> identical bytes
+    a, b = tmp_path / "a", tmp_path / "b"
+    c = run.RunConfig(d=3, g=2.0, dt=0.05, t_max=0.5, scheme="qr_cbe", chi_max=32, checkpoint_every=5)
+    c.out_path = str(a)
+    run.run_quench(c, ctx)
+    c.out_path = str(b)
+    run.run_quench(c, ctx)
+    obs_a = (a / "observables.csv").read_bytes()
+    assert obs_a and obs_a == (b / "observables.csv").read_bytes()
+    assert (a / "bonds.csv").read_bytes() == (b / "bonds.csv").read_bytes()
+    for name in ("config.json", "state.mps", "checkpoint_000005.mps", "checkpoint_000010.mps"):
+        assert (a / name).exists()
+    assert obs_a.decode().split("\n")[0] == "t,site,z_re,z_im"
+    assert (a / "bonds.csv").read_text().split("\n")[0] == "t,bond,entropy,eps_trunc,chi"
+    assert run.config_from_json((a / "config.json").read_text()).chi_max == 32
+    # ten steps x two sites / bonds
+    assert len(obs_a.decode().strip().split("\n")) == 1 + 10 * 2
+
+
+def test_quench_checkpoint_loads_back(ctx, tmp_path):
+    out = tmp_path / "f"
+    c = run.RunConfig(d=2, g=2.0, system_kind="finite", system_size=5, dt=0.05, t_max=0.2, scheme="qr",
+                      chi_max=8, out_path=str(out))
+    res = run.run_quench(c, ctx)
+    st = run.load_mps(str(out / "state.mps"), ctx)
+    assert isinstance(st, q.FiniteMPS) and st.length() == 5
+    z = ref.clock_operators(2)[0]
+    zs, _ = q.finite_observables(st, z)
+    assert np.allclose(zs, res.rows[-1].z, atol=1e-13)
+    host = run.read_checkpoint(str(out / "state.mps"))
+    o = ref.FiniteMPS(2, host["sites"], host["center_bond"], host["center"])
+    for s in range(5):
+        assert abs(ref.expectation_local_finite(o, z, s) - zs[s]) < 1e-12
+    u = tmp_path / "u"
+    run.run_quench(run.RunConfig(d=2, dt=0.05, t_max=0.1, scheme="qr", chi_max=8, out_path=str(u)), ctx)
+    us = run.load_mps(str(u / "state.mps"), ctx)
+    assert isinstance(us, q.UniformMPS) and us.cell_length() == 2
