@@ -250,6 +250,14 @@ qt_status qt_finite_step(qt_finite* f, uint64_t n_layers, const int32_t* parity,
 qt_status qt_finite_observables(const qt_finite* f, const qt_tensor* op, double* z_out, double* schmidt_out,
                                 uint64_t cap, uint64_t* offsets);
 
+/* left_defect, proj/src/mps.cpp:39-41: || sum_i B^i^H B^i - 1 ||_max */
+qt_status qt_left_defect(qt_ctx* ctx, const qt_tensor* b, double* out);
+/* check_isometric(FiniteMPS, tol), proj/src/mps.cpp:143-164: left defects of
+ * the sites left of the center, right defects of the others, | ||C|| - 1 | of
+ * the center matrix; per-site arrays (length n) may be NULL. */
+qt_status qt_check_isometric_finite(const qt_finite* f, double tol, double* right_defects, double* left_defects,
+                                    double* norm_defect, qt_isometry_report* out);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Per-launch CUDA-event profile of the DMMA GEMM kernel (roofline evidence):
  * between begin and end every GEMM launch is bracketed by events; end

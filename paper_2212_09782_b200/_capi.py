@@ -115,6 +115,8 @@ SIGNATURES = {
     "qt_finite_step": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int, C.POINTER(qt_policy),
                                  C.POINTER(qt_bond_report), U64P]),
     "qt_finite_observables": (C.c_int, [P, P, DP, DP, C.c_uint64, U64P]),
+    "qt_left_defect": (C.c_int, [P, P, DP]),
+    "qt_check_isometric_finite": (C.c_int, [P, C.c_double, DP, DP, DP, P]),
     "qt_expectation_local": (C.c_int, [P, P, P, P, DP]),
     "qt_schmidt_values": (C.c_int, [P, P, DP, U64P]),
     "qt_right_defect": (C.c_int, [P, P, DP]),

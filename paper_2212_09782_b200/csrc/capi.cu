@@ -1278,4 +1278,47 @@ qt_status qt_finite_observables(const qt_finite* f, const qt_tensor* op, double*
   return st;
 }
 
+qt_status qt_left_defect(qt_ctx* ctx, const qt_tensor* b, double* out) {
+  return guard([&] {
+    require(ctx && b && out, qt::Err::input, "qt_left_defect: null argument");
+    require_tensor(b, 3, "left_defect");
+    *out = qt::left_defect(ctx->eng, b->data, b->shape[0], b->shape[1], b->shape[2]);
+  });
+}
+
+qt_status qt_check_isometric_finite(const qt_finite* f, double tol, double* right_defects, double* left_defects,
+                                    double* norm_defect, qt_isometry_report* out) {
+  return guard([&] {
+    require(f && out, qt::Err::input, "qt_check_isometric_finite: null argument");
+    qt::Engine& e = f->ctx->eng;
+    const uint64_t n = f->sites.size();
+    double mr = 0.0, ml = 0.0;
+    for (uint64_t s = 0; s < n; ++s) {
+      const qt_tensor* b = f->sites[s];
+      double r = 0.0, l = 0.0;
+      if (s < f->center_bond)
+        l = qt::left_defect(e, b->data, b->shape[0], b->shape[1], b->shape[2]);
+      else
+        r = qt::right_defect(e, b->data, b->shape[0], b->shape[1], b->shape[2]);
+      if (right_defects) right_defects[s] = r;
+      if (left_defects) left_defects[s] = l;
+      mr = std::max(mr, r);
+      ml = std::max(ml, l);
+    }
+    qt::norm2(e, f->center->data, f->center->shape[0], f->center->shape[1], f->center->shape[1],
+              e.dscal + qt::SC_TMP2);
+    double n2 = 0.0;
+    QT_CUDA(cudaMemcpyAsync(&n2, e.dscal + qt::SC_TMP2, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+    QT_CUDA(cudaStreamSynchronize(e.stream));
+    const double nd = std::abs(std::sqrt(n2) - 1.0);
+    if (norm_defect) *norm_defect = nd;
+    out->max_right_defect = mr;
+    out->max_left_defect = ml;
+    out->max_translation_defect = 0.0;
+    out->max_norm_defect = nd;
+    out->pass = std::max(std::max(mr, ml), nd) <= tol ? 1 : 0;
+    out->reserved = 0;
+  });
+}
+
 }  // extern "C"

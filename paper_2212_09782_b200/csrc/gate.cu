@@ -310,6 +310,21 @@ double right_defect(Engine& e, const double2* b, long long d, long long chi_l, l
   return out;
 }
 
+double left_defect(Engine& e, const double2* b, long long d, long long chi_l, long long chi_r) {
+  // sum_i B^i^H B^i - 1 (mps.cpp:39-41): B as a (d chi_l) x chi_r matrix, one Gram GEMM
+  double2* g = e.cbuf(S_MISC, chi_r * chi_r);
+  gemm(e, Op::H, Op::N, chi_r, chi_r, d * chi_l, b, chi_r, b, chi_r, g, chi_r);
+  double* part = e.dbuf(S_NORM_PART, 296);
+  defect_partial_kernel<<<148, 256, 0, e.stream>>>(g, chi_r, part);
+  QT_LAUNCHED();
+  max_final_kernel<<<1, 32, 0, e.stream>>>(part, 148, e.dscal + SC_TMP1);
+  QT_LAUNCHED();
+  double out = 0;
+  QT_CUDA(cudaMemcpyAsync(&out, e.dscal + SC_TMP1, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  return out;
+}
+
 namespace {
 __global__ void maxabs_diff_partial_kernel(const double2* __restrict__ a, const double2* __restrict__ b, long long n,
                                            double* part) {

@@ -96,6 +96,7 @@ std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<
 void expectation_local(Engine& e, const double2* xi, long long xi_rows, long long chi_l, const double2* b,
                        long long d, long long chi_r, const double2* op, double* out2_host);
 double right_defect(Engine& e, const double2* b, long long d, long long chi_l, long long chi_r);
+double left_defect(Engine& e, const double2* b, long long d, long long chi_l, long long chi_r);
 double bond_energy(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
                    const double2* h);
 double explicit_error(Engine& e, const double2* theta, long long rows, long long cols, const double2* left,

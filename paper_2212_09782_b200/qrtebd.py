@@ -564,3 +564,24 @@ def schmidt_values_finite(state: FiniteMPS, bond: int) -> np.ndarray:
         raise InputError("bond out of range")
     c = move_center(state, bond)
     return schmidt_values_of(c.view("center"), c.ctx)
+
+
+def left_defect(b, ctx: Context = None) -> float:
+    """proj/src/mps.cpp:39-41."""
+    ctx = ctx or default_context()
+    t = _dev(ctx, b)
+    out = C.c_double()
+    check(ctx.lib.qt_left_defect(ctx.h, t.h, C.byref(out)))
+    return out.value
+
+
+def check_isometric_finite(state: FiniteMPS, tol: float) -> IsometryReport:
+    """check_isometric(FiniteMPS), proj/src/mps.cpp:143-164, on the device."""
+    n = state.n
+    r = (C.c_double * n)()
+    l = (C.c_double * n)()
+    nd = C.c_double()
+    rep = _capi.qt_isometry_report()
+    check(state.ctx.lib.qt_check_isometric_finite(state.h, tol, r, l, C.byref(nd), C.byref(rep)))
+    return IsometryReport(list(r), list(l), [], [nd.value], rep.max_right_defect, rep.max_left_defect, 0.0,
+                          rep.max_norm_defect, bool(rep.pass_))
