@@ -2,6 +2,8 @@
 // copies).  The permutes replace the reference's ComplexTensor::transpose
 // copies (proj/src/tensor.cpp:100-147) where the layout cannot be folded
 // into a GEMM store.
+#include <cstdlib>
+
 #include "engine.cuh"
 
 namespace qt {
@@ -13,11 +15,17 @@ void Engine::init(int dev, cudaStream_t st) {
   int sms = 0;
   QT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   num_sms = sms;
+  // the context's own stream carries the latency-bound critical path (QR
+  // panels); it gets the highest priority so that CTAs of the side-stream
+  // GEMMs never hold SMs a pending panel cluster is waiting for
+  int prio_least = 0, prio_greatest = 0;
+  QT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+  static const bool no_prio = std::getenv("QT_NO_STREAM_PRIORITY") != nullptr;
   if (st) {
     stream = st;
     own_stream = false;
   } else {
-    QT_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    QT_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, no_prio ? prio_least : prio_greatest));
     own_stream = true;
   }
   QT_CUDA(cudaMalloc(&dscal, SC_COUNT * sizeof(double)));
@@ -26,6 +34,7 @@ void Engine::init(int dev, cudaStream_t st) {
   QT_CUDA(cudaMalloc(&barrier, 64 * sizeof(unsigned)));
   QT_CUDA(cudaMemset(barrier, 0, 64 * sizeof(unsigned)));
   QT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  QT_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
 }
 
 cudaEvent_t Engine::event(size_t i) {
@@ -52,6 +61,11 @@ void Engine::destroy() {
     cudaStreamDestroy(side);
   }
   side = nullptr;
+  if (side2) {
+    cudaStreamSynchronize(side2);
+    cudaStreamDestroy(side2);
+  }
+  side2 = nullptr;
   for (cudaEvent_t ev : events) cudaEventDestroy(ev);
   events.clear();
   dscal = nullptr;
@@ -92,6 +106,17 @@ GemmScratch Engine::gemm_scratch() {
   s.partial_elems = part;
   const size_t ts = size_t(1) << 20;
   s.tile_sums = dbuf(S_TILE_SUMS, ts);
+  s.tile_sums_elems = ts;
+  return s;
+}
+
+GemmScratch Engine::gemm_scratch2() {
+  GemmScratch s;
+  const size_t part = size_t(1) << 22;
+  s.partial = cbuf(S_GEMM_PART2, part);
+  s.partial_elems = part;
+  const size_t ts = size_t(1) << 16;
+  s.tile_sums = dbuf(S_TILE_SUMS2, ts);
   s.tile_sums_elems = ts;
   return s;
 }

@@ -86,14 +86,28 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
 
   // alternating sweep with Y0 = theta[:eta] (gates.cpp:403-404, :293-308)
   const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
+  // Y = Q_m^H theta through the reflectors of QR(X) (see gate_qr_async); theta
+  // becomes Q_full^H theta, Q_m is never formed (CBE keeps no left_iso)
+  const bool qtheta = use_qtheta(pol, rows);
   for (int it = 0; it < sweeps; ++it) {
     if (it == 0)
       gemm2(e, Op::N, Op::H, rows, eta, cols, theta, cols, theta, cols, X, eta);
     else
       gemm2(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);
     check_finite(e, X, rows * eta, flag);
-    qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta);
-    gemm2(e, Op::H, Op::N, cols, eta, rows, theta, cols, Qm, eta, YH, eta);
+    if (qtheta) {
+      QrOpts o;
+      o.capply = theta;
+      o.ldc = cols;
+      o.nc = cols;
+      o.want_q = false;
+      o.want_r = false;
+      qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta, o);
+      qtheta_yh(e, theta, cols, X, eta, YH);
+    } else {
+      qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta);
+      gemm2(e, Op::H, Op::N, cols, eta, rows, theta, cols, Qm, eta, YH, eta);
+    }
     check_finite(e, YH, cols * eta, flag);
     qr_inplace(e, YH, cols, eta, eta, Qp, eta, Rp, eta);
   }
@@ -163,10 +177,15 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
   rep.finite = true;
   if (pol.compute_explicit_error) {
     // center_kept = L V_k V_k^H (gates.cpp:441-444): eps = |theta - Q_m (L V_k) Z^H|^2 / |theta|^2
-    double2* LV = X;  // consumed by the QR above
+    // consumed by the QR above (with qtheta X still carries the gauge phases of
+    // R on its diagonal and the unused Rm holds L V_k instead)
+    double2* LV = qtheta ? Rm : X;
     gemm2(e, Op::H, Op::N, eta, kk, eta, Rp, eta, V, eta, LV, kk);
     double2* W = e.cbuf(S_W, eta * cols);
     gemm2(e, Op::N, Op::H, eta, cols, kk, LV, kk, Z, kk, W, cols);
+    if (qtheta) {
+      qtheta_resid(e, theta, rows, cols, X, eta, W, e.dscal + SC_RESID);
+    } else {
     GemmDesc g;
     g.M = rows;
     g.N = cols;
@@ -179,6 +198,7 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
     g.ldc = cols;
     g.mode = GemmMode::resid;
     zgemm(g, e.gemm_scratch(), e.stream, e.dscal + SC_RESID);
+    }
     double r = 0.0;
     QT_CUDA(cudaMemcpyAsync(&r, e.dscal + SC_RESID, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
     QT_CUDA(cudaStreamSynchronize(e.stream));

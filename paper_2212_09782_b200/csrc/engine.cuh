@@ -37,6 +37,11 @@ enum Slot : int {
   S_MISC,
   S_MISC2,
   S_REPORTS,
+  S_QA_W,        // W = V^H C of the reflector application to a second matrix (QrOpts::capply)
+  S_QA_W2,
+  S_GEMM_PART2,  // split-K partials of GEMMs on the second side stream
+  S_TILE_SUMS2,
+  S_QT_PART,     // partial sums of the Q^H theta residual
   S_COUNT
 };
 
@@ -66,6 +71,9 @@ struct Engine {
   // (the QR trailing update behind the next panel); forks and joins through
   // events, so it is captured into CUDA graphs with the main stream
   cudaStream_t side = nullptr;
+  // third stream: applies each finished panel's block reflector to a second
+  // matrix (Q^H theta) behind the panel chain (QrOpts::capply)
+  cudaStream_t side2 = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t event(size_t i);
 
@@ -76,6 +84,7 @@ struct Engine {
   double2* cbuf(int slot, size_t elems) { return static_cast<double2*>(raw(slot, elems * sizeof(double2))); }
   double* dbuf(int slot, size_t elems) { return static_cast<double*>(raw(slot, elems * sizeof(double))); }
   GemmScratch gemm_scratch();
+  GemmScratch gemm_scratch2();  // separate split-K buffers for GEMMs on side2
 };
 
 // ---- kernels shared by the modules (aux.cu) -------------------------------
@@ -95,7 +104,16 @@ void check_finite(Engine& e, const double2* x, long long n, int* dflag);
 // in place (a is destroyed).  Writes the explicit thin Q (m x k, ld ldq) and
 // R (k x n, ld ldr), k = min(m, n), gauge-fixed so that diag(R) is real and
 // non-negative (proj/src/linalg.cpp:25-51).
+struct QrOpts {
+  // when set: C (m x nc, ld ldc) <- Q^H C, applied panel by panel on e.side2
+  // while the later panels factor (the reflectors are complete when qr_inplace
+  // returns; the caller's stream has joined side2)
+  double2* capply = nullptr;
+  long long ldc = 0, nc = 0;
+  bool want_q = true;  // form the explicit thin Q (gauge-fixed)
+  bool want_r = true;  // write the gauge-fixed R
+};
 void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, double2* q, long long ldq,
-                double2* r, long long ldr);
+                double2* r, long long ldr, const QrOpts& opts = QrOpts());
 
 }  // namespace qt

@@ -14,6 +14,7 @@
 //   Xi~ = L/|L|, B~n = Q_n -> (d,eta,chi_r), B~m = phiev Q_n^H (permuted store),
 //   left_iso = Q_m -> (d,chi_l,eta), eps = ||theta - Q_m L Q_n||^2/||theta||^2
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "gate.cuh"
@@ -49,6 +50,73 @@ __global__ void inv_norm_kernel(double* dscal, int a, int b, int skip, int out) 
 }
 
 __global__ void zero_flag_kernel(int* f) { *f = 0; }
+
+// gauge phase of reflector column i: R_ii / |R_ii| (1 when R_ii == 0), the
+// phase gauge_q applies to column i of Q (proj/src/linalg.cpp:25-36)
+__device__ __forceinline__ double2 qr_phase(const double2* __restrict__ a, long long lda, long long i) {
+  const double2 d = a[i * lda + i];
+  const double ad = hypot(d.x, d.y);
+  return ad == 0.0 ? make_double2(1.0, 0.0) : make_double2(d.x / ad, d.y / ad);
+}
+
+// Y^H from Q_full^H theta: yh[c, i] = ph_i conj(qt[i, c]) for i < eta, i.e.
+// Y = Q_m^H theta with the gauge-fixed Q_m = Q_raw diag(ph)  (32 x 32 tiles)
+__global__ void yh_gauge_kernel(const double2* __restrict__ qt, long long cols, const double2* __restrict__ a,
+                                long long lda, long long eta, double2* __restrict__ yh) {
+  __shared__ double2 tile[32][33];
+  const long long i0 = static_cast<long long>(blockIdx.y) * 32, c0 = static_cast<long long>(blockIdx.x) * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const long long i = i0 + r, c = c0 + threadIdx.x;
+    if (i < eta && c < cols) {
+      const double2 v = qt[i * cols + c];
+      const double2 ph = qr_phase(a, lda, i);
+      tile[r][threadIdx.x] = cmul(ph, cconj(v));
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const long long c = c0 + r, i = i0 + threadIdx.x;
+    if (c < cols && i < eta) yh[c * eta + i] = tile[threadIdx.x][r];
+  }
+}
+
+// explicit truncation error from Q_full^H theta (gates.cpp:464-485 by unitary
+// invariance): ||theta - Q_m W||^2 = ||Y - W||^2 + ||Z||^2 with Y (gauged) the
+// first eta rows of Q_full^H theta, Z the rest and W = L Q_n; fixed-order
+// two-pass reduction
+__global__ void qtheta_resid_partial_kernel(const double2* __restrict__ qt, long long rows, long long cols,
+                                            const double2* __restrict__ a, long long lda, long long eta,
+                                            const double2* __restrict__ w, double* part) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  const long long total = rows * cols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / cols;
+    double2 v = qt[e];
+    if (i < eta) v = csub(cmul(cconj(qr_phase(a, lda, i)), v), w[e]);
+    s = fma(v.x, v.x, fma(v.y, v.y, s));
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// one warp: lane l sums part[l], part[l + 32], ... in order, then a fixed
+// shuffle tree (deterministic; the loads of all lanes issue in parallel)
+__global__ void sum_final_kernel(const double* __restrict__ part, int n, double* out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) s += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) *out = s;
+}
+
+constexpr int kResidBlocks = 296;
 
 __global__ void trace_op_kernel(const double2* __restrict__ op, const double2* __restrict__ t2, int d,
                                 double* out2) {
@@ -136,6 +204,28 @@ void gemm(Engine& e, Op oa, Op ob, long long M, long long N, long long K, const 
 
 }  // namespace
 
+bool use_qtheta(const qt_policy& pol, long long rows) {
+  static const long long qtheta_max = std::getenv("QT_QTHETA_MAX_ROWS")
+                                          ? std::atoll(std::getenv("QT_QTHETA_MAX_ROWS"))
+                                          : 2048;
+  return std::max(1, static_cast<int>(pol.qr_sweeps)) == 1 && rows <= qtheta_max;
+}
+
+void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh) {
+  dim3 tg(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(eta, 32)));
+  yh_gauge_kernel<<<tg, dim3(32, 8), 0, e.stream>>>(qt, cols, a, eta, eta, yh);
+  QT_LAUNCHED();
+}
+
+void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, const double2* a, long long eta,
+                  const double2* w, double* out) {
+  double* part = e.dbuf(S_QT_PART, kResidBlocks);
+  qtheta_resid_partial_kernel<<<kResidBlocks, 256, 0, e.stream>>>(qt, rows, cols, a, eta, eta, w, part);
+  QT_LAUNCHED();
+  sum_final_kernel<<<1, 32, 0, e.stream>>>(part, kResidBlocks, out);
+  QT_LAUNCHED();
+}
+
 void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
                  const double2* u, int out_scalar) {
   const long long d = D.d, cl = D.chi_l, cm = D.chi_m, cn = D.chi_n, cr = D.chi_r;
@@ -196,14 +286,32 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     y0 = y;
   }
   const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
+  // Y = Q_m^H theta through the reflectors (one sweep, theta up to
+  // QT_QTHETA_MAX_ROWS rows): each finished panel of QR(X) is applied to theta
+  // on a side stream while the later panels factor, so when the panel chain
+  // ends Q_full^H theta = [Y; Z] is ready -- no explicit Q_m (unless left_iso
+  // is wanted), no theta^H Q_m GEMM, and the explicit error needs only
+  // ||Y - L Q_n||^2 + ||Z||^2 instead of a theta-sized residual product
+  const bool qtheta = use_qtheta(pol, rows);
   for (int it = 0; it < sweeps; ++it) {
     if (it == 0)
       gemm(e, Op::N, Op::H, rows, eta, cols, theta, cols, y0, cols, X, eta);  // X = theta Y0^H
     else
       gemm(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);   // Y0 = Q_n = Qp^H
     check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
-    qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta);
-    gemm(e, Op::H, Op::N, cols, eta, rows, theta, cols, Qm, eta, YH, eta);  // Y^H = theta^H Q_m
+    if (qtheta) {
+      QrOpts o;
+      o.capply = theta;  // theta <- Q_full^H theta (theta is not read again: ||theta|| is already known)
+      o.ldc = cols;
+      o.nc = cols;
+      o.want_q = out.left_iso != nullptr;
+      o.want_r = false;
+      qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta, o);
+      qtheta_yh(e, theta, cols, X, eta, YH);
+    } else {
+      qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta);
+      gemm(e, Op::H, Op::N, cols, eta, rows, theta, cols, Qm, eta, YH, eta);  // Y^H = theta^H Q_m
+    }
     check_finite(e, YH, cols * eta, flag);
     qr_inplace(e, YH, cols, eta, eta, Qp, eta, Rp, eta);  // Y^H = Qp Rp -> L = Rp^H, Q_n = Qp^H
   }
@@ -240,7 +348,12 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     const int perm[3] = {1, 0, 2};
     permute(e, Qm, 3, shp, perm, false, out.left_iso);
   }
-  if (pol.compute_explicit_error) {
+  if (pol.compute_explicit_error && qtheta) {
+    // W = L Q_n = Rp^H Qp^H (eta x cols); ||theta - Q_m W||^2 = ||Y - W||^2 + ||Z||^2
+    double2* W = e.cbuf(S_W, eta * cols);
+    gemm(e, Op::H, Op::H, eta, cols, eta, Rp, eta, Qp, eta, W, cols);
+    qtheta_resid(e, theta, rows, cols, X, eta, W, e.dscal + SC_RESID);
+  } else if (pol.compute_explicit_error) {
     // W = L Q_n = Rp^H Qp^H (eta x cols), then sum |theta - Q_m W|^2 (gates.cpp:464-485)
     double2* W = e.cbuf(S_W, eta * cols);
     gemm(e, Op::H, Op::H, eta, cols, eta, Rp, eta, Qp, eta, W, cols);

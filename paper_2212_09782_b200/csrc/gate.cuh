@@ -49,6 +49,16 @@ void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm,
 void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
                    const double2* u, const qt_policy& pol, long long eta, const GateBuffers& out);
 
+// Y = Q_m^H theta through the reflectors of QR(X) (QrOpts::capply): used for
+// one sweep on matrices up to QT_QTHETA_MAX_ROWS rows (default 2048)
+bool use_qtheta(const qt_policy& pol, long long rows);
+// Y^H (cols x eta) from Q_full^H theta (rows x cols) with the gauge phases of
+// the factored X (diag of a, ld eta)
+void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh);
+// *out = ||Y - W||^2 + ||Z||^2 = ||theta - Q_m W||^2 (W: eta x cols), fixed-order reduction
+void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, const double2* a, long long eta,
+                  const double2* w, double* out);
+
 // Collects the report of the last gate_qr_async / CBE update (synchronizes).
 HostReport read_report(Engine& e);
 

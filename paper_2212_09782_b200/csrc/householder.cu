@@ -366,10 +366,36 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp) {
   QT_LAUNCHED();
 }
 
+// C <- H_p^H C = C - V T^H (V^H C) on stream st (three DMMA GEMMs; W/W2 and the
+// split-K scratch belong to that stream)
+void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, double2* C, long long ldc,
+                           long long mp, long long nc, int nbp, double2* W, double2* W2, const GemmScratch& gs,
+                           cudaStream_t st) {
+  GemmDesc g;
+  g.M = nbp; g.N = nc; g.K = mp;
+  g.opA = Op::H; g.A = Vp; g.lda = ldv;
+  g.opB = Op::N; g.B = C; g.ldb = ldc;
+  g.C = W; g.ldc = nc;
+  zgemm(g, gs, st);
+  GemmDesc g2;
+  g2.M = nbp; g2.N = nc; g2.K = nbp;
+  g2.opA = Op::H; g2.A = Tp; g2.lda = NB;
+  g2.opB = Op::N; g2.B = W; g2.ldb = nc;
+  g2.C = W2; g2.ldc = nc;
+  zgemm(g2, gs, st);
+  GemmDesc g3;
+  g3.M = mp; g3.N = nc; g3.K = nbp;
+  g3.opA = Op::N; g3.A = Vp; g3.lda = ldv;
+  g3.opB = Op::N; g3.B = W2; g3.ldb = nc;
+  g3.C = C; g3.ldc = ldc;
+  g3.alpha = -1.0; g3.beta = 1.0;
+  zgemm(g3, gs, st);
+}
+
 }  // namespace
 
 void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, double2* q, long long ldq,
-                double2* r, long long ldr) {
+                double2* r, long long ldr, const QrOpts& opts) {
   const long long k = std::min(m, n);
   if (k == 0) return;
   const long long npan = ceil_div(k, NB);
@@ -399,6 +425,17 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   const bool lookahead = la_env && npan >= 2 && e.side != nullptr && larfb_cluster_fits(m);
   bool wide_pending = false;
   long long last_wide = -1;
+  // QrOpts::capply: panel p's reflector reaches C on side2 once the panel is
+  // factored (events 2 npan + p), concurrently with the later panels
+  const bool capply = opts.capply != nullptr && opts.nc > 0;
+  const size_t cev = static_cast<size_t>(2 * npan + 2);
+  double2 *CW = nullptr, *CW2 = nullptr;
+  GemmScratch gs2;
+  if (capply) {
+    CW = e.cbuf(S_QA_W, static_cast<size_t>(NB) * opts.nc);
+    CW2 = e.cbuf(S_QA_W2, static_cast<size_t>(NB) * opts.nc);
+    gs2 = e.gemm_scratch2();
+  }
   for (long long p = 0; p < npan; ++p) {
     const long long j = p * NB;
     const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
@@ -410,6 +447,15 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
     pa.V = V + j * kp + p * NB;
     pa.T = T + p * NB * NB;
     launch_panel(e, pa, mp);
+    if (capply) {
+      QT_CUDA(cudaEventRecord(e.event(cev + p), e.stream));
+      QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(cev + p), 0));
+      static const bool cl_apply = std::getenv("QT_QTHETA_CLUSTER") != nullptr;
+      if (!cl_apply || !larfb_cluster(e, pa.V, kp, pa.T, opts.capply + j * opts.ldc, opts.ldc, mp, opts.nc, nbp, true,
+                                      e.side2))
+        apply_block_reflector(pa.V, kp, pa.T, opts.capply + j * opts.ldc, opts.ldc, mp, opts.nc, nbp, CW, CW2, gs2,
+                              e.side2);
+    }
     if (dbg_on) {
       long long h[8 * NB];
       QT_CUDA(cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, e.stream));
@@ -473,6 +519,17 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   }
 
   if (last_wide >= 0) QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(2 * last_wide + 1), 0));  // join the side stream
+  if (capply) {  // join side2: Q^H C complete
+    QT_CUDA(cudaEventRecord(e.event(cev + npan), e.side2));
+    QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(cev + npan), 0));
+  }
+  if (!opts.want_q) {
+    if (opts.want_r) {
+      gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
+      QT_LAUNCHED();
+    }
+    return;
+  }
 
   // explicit thin Q = H_0 ... H_{k-1} I[:, :k], block reflectors backward
   set_identity(e, q, m, k, ldq);
@@ -507,8 +564,10 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 
   gauge_q_kernel<<<grid_for(m * k), 256, 0, e.stream>>>(a, lda, q, ldq, m, k);
   QT_LAUNCHED();
-  gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
-  QT_LAUNCHED();
+  if (opts.want_r) {
+    gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
+    QT_LAUNCHED();
+  }
 }
 
 }  // namespace qt

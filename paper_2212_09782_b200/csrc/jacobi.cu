@@ -60,6 +60,7 @@ struct JacobiArgs {
   int N, nb;
   int full_inner;  // 1: full inner sweep in every outer round (QT_JACOBI_FULL)
   double tol;
+  double abs_floor;  // rotations skipped below abs_floor * ||G||_F
   int* sweeps_out;
   long long* prof;  // optional: cycles of CTA 0 in phase A / flag waits / phase B / first wave + barrier
   unsigned* tflag;  // [P(P+1)/2] round counter of the last update of every G pair tile
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   const int N = a.N;
   const int ngt = P * (P + 1) / 2, nvt = (N / JX) * P;
   const double sc = jscale(a.fro2);
-  const double abs_tol = 1e-22 * sqrt(*a.fro2) * sc;
+  const double abs_tol = a.abs_floor * sqrt(*a.fro2) * sc;
   const double abs_tol2 = abs_tol * abs_tol, tol2 = a.tol * a.tol;
   const bool stamp = a.prof && tid == 0 && cta == 0;
   long long pa = 0, pw = 0, pb = 0, ps = 0;
@@ -574,7 +575,8 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   if (n <= 0) return;
   // 16-wide blocks (32x32 subproblems) below n = 512, 32-wide above: the
   // subproblem sweep is the critical path for small n, the tile updates for large n
-  const int JB = n <= 512 ? 16 : 32, JX = 2 * JB, JT = 16 * JB;
+  static const int jb_env = std::getenv("QT_JACOBI_JB") ? std::atoi(std::getenv("QT_JACOBI_JB")) : 0;
+  const int JB = jb_env == 16 || jb_env == 32 ? jb_env : (n <= 512 ? 16 : 32), JX = 2 * JB, JT = 16 * JB;
   int nb = static_cast<int>(ceil_div(n, JB));
   if (nb < 2) nb = 2;
   if (nb & 1) ++nb;
@@ -606,6 +608,8 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   a.N = N;
   a.nb = nb;
   a.tol = 2.220446049250313e-16;  // relative off-diagonal threshold (unit roundoff)
+  static const double abs_floor = std::getenv("QT_JACOBI_ABS") ? std::atof(std::getenv("QT_JACOBI_ABS")) : 1e-22;
+  a.abs_floor = abs_floor;
   static const bool full_inner = std::getenv("QT_JACOBI_FULL") != nullptr;
   a.full_inner = full_inner ? 1 : 0;
   a.sweeps_out = sweeps;
