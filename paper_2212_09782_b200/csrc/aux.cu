@@ -35,6 +35,7 @@ void Engine::init(int dev, cudaStream_t st) {
   QT_CUDA(cudaMemset(barrier, 0, 64 * sizeof(unsigned)));
   QT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   QT_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+  QT_CUDA(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, no_prio ? prio_least : prio_greatest));
 }
 
 cudaEvent_t Engine::event(size_t i) {
@@ -66,6 +67,11 @@ void Engine::destroy() {
     cudaStreamDestroy(side2);
   }
   side2 = nullptr;
+  if (side3) {
+    cudaStreamSynchronize(side3);
+    cudaStreamDestroy(side3);
+  }
+  side3 = nullptr;
   for (cudaEvent_t ev : events) cudaEventDestroy(ev);
   events.clear();
   dscal = nullptr;
@@ -294,9 +300,9 @@ void copy2d(Engine& e, const double2* src, long long lds, double2* dst, long lon
   QT_LAUNCHED();
 }
 
-void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld) {
+void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld, cudaStream_t st) {
   if (rows * cols == 0) return;
-  identity_kernel<<<grid_for(rows * cols), 256, 0, e.stream>>>(q, rows, cols, ld);
+  identity_kernel<<<grid_for(rows * cols), 256, 0, st ? st : e.stream>>>(q, rows, cols, ld);
   QT_LAUNCHED();
 }
 

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -42,6 +43,8 @@ enum Slot : int {
   S_GEMM_PART2,  // split-K partials of GEMMs on the second side stream
   S_TILE_SUMS2,
   S_QT_PART,     // partial sums of the Q^H theta residual
+  S_QR_V2,       // reflectors / T factors of the second QR of a pipelined pair
+  S_QR_T2,
   S_COUNT
 };
 
@@ -74,6 +77,8 @@ struct Engine {
   // third stream: applies each finished panel's block reflector to a second
   // matrix (Q^H theta) behind the panel chain (QrOpts::capply)
   cudaStream_t side2 = nullptr;
+  // fourth stream: the second QR of a pipelined pair (qr_pair_pipelined)
+  cudaStream_t side3 = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t event(size_t i);
 
@@ -96,7 +101,7 @@ void norm2(Engine& e, const double2* x, long long rows, long long cols, long lon
 // dst = src over rows x cols blocks with leading dimensions
 void copy2d(Engine& e, const double2* src, long long lds, double2* dst, long long ldd, long long rows,
             long long cols);
-void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld);
+void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld, cudaStream_t st = nullptr);
 void check_finite(Engine& e, const double2* x, long long n, int* dflag);
 
 // ---- Householder QR (householder.cu) ----------------------------------------
@@ -115,5 +120,22 @@ struct QrOpts {
 };
 void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, double2* q, long long ldq,
                 double2* r, long long ldr, const QrOpts& opts = QrOpts());
+
+// The two QRs of one alternating sweep (proj/src/gates.cpp:293-308), pipelined:
+//   QR(X), X (m x k) -- every finished panel p is applied to C (m x nc) on
+//   e.side2, so C <- Q_full^H C, and then `extract(r0, nr, stream)` publishes
+//   rows [r0, r0 + nr) of C, which are final, as columns of Y^H (nc x k);
+//   QR(Y^H) on e.side3 runs one panel behind: panel p of Y^H starts once block
+//   p is extracted and has received the reflectors of Y^H panels < p
+//   (left-looking block update).
+// Only the explicit thin Q of Y^H (qy, nc x k) and its R (ry, k x k) are
+// formed, gauge-fixed; X keeps its factored form (R on the upper triangle,
+// the gauge phases on the diagonal).  Requires k <= m, k <= nc and both
+// heights within one block-reflector cluster (qr_pair_fits).  Everything is
+// joined into e.stream on return.
+bool qr_pair_fits(long long m, long long nc);
+void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
+                       double2* qy, double2* ry,
+                       const std::function<void(long long, long long, cudaStream_t)>& extract);
 
 }  // namespace qt

@@ -61,13 +61,14 @@ __device__ __forceinline__ double2 qr_phase(const double2* __restrict__ a, long 
 
 // Y^H from Q_full^H theta: yh[c, i] = ph_i conj(qt[i, c]) for i < eta, i.e.
 // Y = Q_m^H theta with the gauge-fixed Q_m = Q_raw diag(ph)  (32 x 32 tiles)
+// (rows [ibeg, iend) of qt; yh and the factored X share the leading dimension lda = eta)
 __global__ void yh_gauge_kernel(const double2* __restrict__ qt, long long cols, const double2* __restrict__ a,
-                                long long lda, long long eta, double2* __restrict__ yh) {
+                                long long lda, long long iend, double2* __restrict__ yh, long long ibeg) {
   __shared__ double2 tile[32][33];
-  const long long i0 = static_cast<long long>(blockIdx.y) * 32, c0 = static_cast<long long>(blockIdx.x) * 32;
+  const long long i0 = ibeg + static_cast<long long>(blockIdx.y) * 32, c0 = static_cast<long long>(blockIdx.x) * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const long long i = i0 + r, c = c0 + threadIdx.x;
-    if (i < eta && c < cols) {
+    if (i < iend && c < cols) {
       const double2 v = qt[i * cols + c];
       const double2 ph = qr_phase(a, lda, i);
       tile[r][threadIdx.x] = cmul(ph, cconj(v));
@@ -76,7 +77,7 @@ __global__ void yh_gauge_kernel(const double2* __restrict__ qt, long long cols, 
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const long long c = c0 + r, i = i0 + threadIdx.x;
-    if (c < cols && i < eta) yh[c * eta + i] = tile[threadIdx.x][r];
+    if (c < cols && i < iend) yh[c * lda + i] = tile[threadIdx.x][r];
   }
 }
 
@@ -211,10 +212,17 @@ bool use_qtheta(const qt_policy& pol, long long rows) {
   return std::max(1, static_cast<int>(pol.qr_sweeps)) == 1 && rows <= qtheta_max;
 }
 
-void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh) {
-  dim3 tg(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(eta, 32)));
-  yh_gauge_kernel<<<tg, dim3(32, 8), 0, e.stream>>>(qt, cols, a, eta, eta, yh);
+void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh,
+               long long ibeg, long long iend, cudaStream_t st) {
+  if (iend < 0) iend = eta;
+  dim3 tg(static_cast<unsigned>(ceil_div(cols, 32)), static_cast<unsigned>(ceil_div(iend - ibeg, 32)));
+  yh_gauge_kernel<<<tg, dim3(32, 8), 0, st ? st : e.stream>>>(qt, cols, a, eta, iend, yh, ibeg);
   QT_LAUNCHED();
+}
+
+bool use_qr_pair(long long rows, long long cols) {
+  static const bool off = std::getenv("QT_NO_QR_PAIR") != nullptr;
+  return !off && qr_pair_fits(rows, cols);
 }
 
 void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, const double2* a, long long eta,
@@ -299,6 +307,15 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     else
       gemm(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);   // Y0 = Q_n = Qp^H
     check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
+    if (qtheta && !out.left_iso && use_qr_pair(rows, cols)) {
+      // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
+      qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp,
+                        [&](long long r0, long long nr, cudaStream_t st) {
+                          qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st);
+                        });
+      check_finite(e, theta, eta * cols, flag);  // Y (the first eta rows of Q_full^H theta)
+      continue;
+    }
     if (qtheta) {
       QrOpts o;
       o.capply = theta;  // theta <- Q_full^H theta (theta is not read again: ||theta|| is already known)

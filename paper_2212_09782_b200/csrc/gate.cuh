@@ -54,7 +54,12 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
 bool use_qtheta(const qt_policy& pol, long long rows);
 // Y^H (cols x eta) from Q_full^H theta (rows x cols) with the gauge phases of
 // the factored X (diag of a, ld eta)
-void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh);
+// (rows [ibeg, iend) only, on stream st; iend < 0: all eta rows, st null: e.stream)
+void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh,
+               long long ibeg = 0, long long iend = -1, cudaStream_t st = nullptr);
+// the two QRs of the sweep run as a pipelined pair (qr_pair_pipelined) when
+// both heights fit one block-reflector cluster (QT_NO_QR_PAIR disables it)
+bool use_qr_pair(long long rows, long long cols);
 // *out = ||Y - W||^2 + ||Z||^2 = ||theta - Q_m W||^2 (W: eta x cols), fixed-order reduction
 void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, const double2* a, long long eta,
                   const double2* w, double* out);

@@ -251,7 +251,7 @@ int grid_for(long long total) {
 
 // returns false when the panel is too tall for one cluster's shared memory
 template <int RPW>
-void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs) {
+void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs, cudaStream_t st) {
   auto kern = panel_cluster_kernel<RPW>;
   static bool attr = false;
   if (!attr) {
@@ -264,7 +264,7 @@ void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs) {
   cfg.gridDim = dim3(static_cast<unsigned>(cs));
   cfg.blockDim = dim3(CL_THREADS);
   cfg.dynamicSmemBytes = panel_cluster_smem(RPW);
-  cfg.stream = e.stream;
+  cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = static_cast<unsigned>(cs);
@@ -276,7 +276,7 @@ void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs) {
   QT_LAUNCHED();
 }
 
-bool launch_panel_cluster(Engine& e, const PanelArgs& base, long long mp) {
+bool launch_panel_cluster(Engine& e, const PanelArgs& base, long long mp, cudaStream_t st) {
   static int max_cs = -1;
   if (max_cs < 0) {
     auto kern = panel_cluster_kernel<CL_MAX_RPW>;
@@ -323,19 +323,20 @@ bool launch_panel_cluster(Engine& e, const PanelArgs& base, long long mp) {
   PanelArgs a = base;
   a.rpc = rpw * CL_WARPS;
   switch (rpw) {
-    case 2: launch_panel_rpw<2>(e, a, cs); break;
-    case 3: launch_panel_rpw<3>(e, a, cs); break;
-    case 5: launch_panel_rpw<5>(e, a, cs); break;
-    case 8: launch_panel_rpw<8>(e, a, cs); break;
-    case 10: launch_panel_rpw<10>(e, a, cs); break;
-    case 14: launch_panel_rpw<14>(e, a, cs); break;
-    default: launch_panel_rpw<CL_MAX_RPW>(e, a, cs); break;
+    case 2: launch_panel_rpw<2>(e, a, cs, st); break;
+    case 3: launch_panel_rpw<3>(e, a, cs, st); break;
+    case 5: launch_panel_rpw<5>(e, a, cs, st); break;
+    case 8: launch_panel_rpw<8>(e, a, cs, st); break;
+    case 10: launch_panel_rpw<10>(e, a, cs, st); break;
+    case 14: launch_panel_rpw<14>(e, a, cs, st); break;
+    default: launch_panel_rpw<CL_MAX_RPW>(e, a, cs, st); break;
   }
   return true;
 }
 
-void launch_panel(Engine& e, const PanelArgs& base, long long mp) {
-  if (launch_panel_cluster(e, base, mp)) return;
+void launch_panel(Engine& e, const PanelArgs& base, long long mp, cudaStream_t st = nullptr) {
+  if (!st) st = e.stream;
+  if (launch_panel_cluster(e, base, mp, st)) return;
   // grid-wide fallback for very tall panels: ~128 rows per CTA, at most one
   // CTA per SM (co-residency for the grid barrier), at least 32 rows so CTA 0
   // owns the whole diagonal block
@@ -356,7 +357,7 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp) {
   cfg.gridDim = dim3(static_cast<unsigned>(G));
   cfg.blockDim = dim3(PANEL_THREADS);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = e.stream;
+  cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeCooperative;
   attrs[0].val.cooperative = 1;
@@ -568,6 +569,115 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
     gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
     QT_LAUNCHED();
   }
+}
+
+
+bool qr_pair_fits(long long m, long long nc) { return larfb_cluster_fits(m) && larfb_cluster_fits(nc); }
+
+void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
+                       double2* qy, double2* ry,
+                       const std::function<void(long long, long long, cudaStream_t)>& extract) {
+  if (k == 0) return;
+  if (k > m || k > nc || !qr_pair_fits(m, nc)) throw Error(Err::internal, "qr_pair_pipelined: shape not supported");
+  const long long npan = ceil_div(k, NB);
+  const long long kp = npan * NB;
+  // X: reflectors in S_QR_V / S_QR_T, Y^H: S_QR_V2 / S_QR_T2 (both QRs are in flight at once)
+  double2* Vx = e.cbuf(S_QR_V, static_cast<size_t>(m) * kp);
+  double2* Tx = e.cbuf(S_QR_T, static_cast<size_t>(npan) * NB * NB);
+  double2* Vy = e.cbuf(S_QR_V2, static_cast<size_t>(nc) * kp);
+  double2* Ty = e.cbuf(S_QR_T2, static_cast<size_t>(npan) * NB * NB);
+  double2* part = e.cbuf(S_QR_PART, static_cast<size_t>(2) * kNumSMs * NB + 2 * NB);
+  double2* CW = e.cbuf(S_QA_W, static_cast<size_t>(NB) * nc);
+  double2* CW2 = e.cbuf(S_QA_W2, static_cast<size_t>(NB) * nc);
+  const GemmScratch gs2 = e.gemm_scratch2();
+  const cudaStream_t sx = e.stream, sxw = e.side, sa = e.side2, sy = e.side3;
+  // events: X look-ahead 2p / 2p+1, panel done P0 + p, block extracted E0 + p, joins J0..
+  const size_t P0 = static_cast<size_t>(2 * npan + 2), E0 = P0 + npan + 1, J0 = E0 + npan + 1;
+
+  PanelArgs base{};
+  base.part = part;
+  base.diag = part + 2 * kNumSMs * NB;
+  base.bar = e.barrier;
+  base.dbg = nullptr;
+
+  // the Y chain may only start after everything earlier on the caller's stream
+  QT_CUDA(cudaEventRecord(e.event(J0), sx));
+  QT_CUDA(cudaStreamWaitEvent(sy, e.event(J0), 0));
+
+  bool wide_pending = false;
+  long long last_wide = -1;
+  for (long long p = 0; p < npan; ++p) {
+    const long long j = p * NB;
+    const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+    // ---- X: panel p (look-ahead as in qr_inplace)
+    PanelArgs pa = base;
+    pa.A = x + j * k + j;
+    pa.lda = k;
+    pa.mp = m - j;
+    pa.nbp = nbp;
+    pa.V = Vx + j * kp + p * NB;
+    pa.ldv = kp;
+    pa.T = Tx + p * NB * NB;
+    launch_panel(e, pa, m - j, sx);
+    // ---- theta side: C <- H_p^H C, then rows [j, j + nbp) of C are final
+    QT_CUDA(cudaEventRecord(e.event(P0 + p), sx));
+    QT_CUDA(cudaStreamWaitEvent(sa, e.event(P0 + p), 0));
+    apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa);
+    extract(j, nbp, sa);
+    QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
+    // ---- X trailing update (look-ahead: next panel's columns on sx, the rest on sxw)
+    const long long ntr = k - j - nbp;
+    if (ntr > 0) {
+      const long long nn = std::min<long long>(NB, ntr);
+      if (p > 0 && wide_pending) QT_CUDA(cudaStreamWaitEvent(sx, e.event(2 * (p - 1) + 1), 0));
+      if (ntr > nn) {
+        QT_CUDA(cudaEventRecord(e.event(2 * p), sx));
+        QT_CUDA(cudaStreamWaitEvent(sxw, e.event(2 * p), 0));
+      }
+      larfb_cluster(e, pa.V, kp, pa.T, x + j * k + j + nbp, k, m - j, nn, nbp, true, sx);
+      wide_pending = ntr > nn;
+      if (wide_pending) {
+        larfb_cluster(e, pa.V, kp, pa.T, x + j * k + j + nbp + nn, k, m - j, ntr - nn, nbp, true, sxw);
+        QT_CUDA(cudaEventRecord(e.event(2 * p + 1), sxw));
+        last_wide = p;
+      }
+    }
+    // ---- Y^H: block p receives the reflectors of Y panels < p, then panel p
+    QT_CUDA(cudaStreamWaitEvent(sy, e.event(E0 + p), 0));
+    for (long long q = 0; q < p; ++q) {
+      const long long jq = q * NB;
+      const int nbq = static_cast<int>(std::min<long long>(NB, k - jq));
+      larfb_cluster(e, Vy + jq * kp + q * NB, kp, Ty + q * NB * NB, yh + jq * k + j, k, nc - jq, nbp, nbq, true, sy);
+    }
+    PanelArgs py = base;
+    py.A = yh + j * k + j;
+    py.lda = k;
+    py.mp = nc - j;
+    py.nbp = nbp;
+    py.V = Vy + j * kp + p * NB;
+    py.ldv = kp;
+    py.T = Ty + p * NB * NB;
+    launch_panel(e, py, nc - j, sy);
+  }
+  // join the X side streams (R of X is not needed; its diagonal carries the gauge phases)
+  if (last_wide >= 0) QT_CUDA(cudaStreamWaitEvent(sx, e.event(2 * last_wide + 1), 0));
+  QT_CUDA(cudaEventRecord(e.event(J0 + 1), sa));
+  QT_CUDA(cudaStreamWaitEvent(sx, e.event(J0 + 1), 0));
+  // explicit thin Q of Y^H = H'_0 ... H'_{k-1} I[:, :k] (backward block reflectors) on sy
+  set_identity(e, qy, nc, k, k, sy);
+  for (long long p = npan - 1; p >= 0; --p) {
+    const long long j = p * NB;
+    const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+    if (!larfb_cluster(e, Vy + j * kp + p * NB, kp, Ty + p * NB * NB, qy + j * k + j, k, nc - j, k - j, nbp, false,
+                       sy))
+      throw Error(Err::internal, "qr_pair_pipelined: block reflector does not fit a cluster");
+  }
+  gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
+  QT_LAUNCHED();
+  gauge_r_kernel<<<grid_for(k * k), 256, 0, sy>>>(yh, k, ry, k, k, k);
+  QT_LAUNCHED();
+  QT_CUDA(cudaEventRecord(e.event(J0 + 2), sy));
+  QT_CUDA(cudaStreamWaitEvent(sx, e.event(J0 + 2), 0));
 }
 
 }  // namespace qt
