@@ -644,11 +644,14 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     }
     // ---- Y^H: block p receives the reflectors of Y panels < p, then panel p
     QT_CUDA(cudaStreamWaitEvent(sy, e.event(E0 + p), 0));
-    for (long long q = 0; q < p; ++q) {
-      const long long jq = q * NB;
-      const int nbq = static_cast<int>(std::min<long long>(NB, k - jq));
-      larfb_cluster(e, Vy + jq * kp + q * NB, kp, Ty + q * NB * NB, yh + jq * k + j, k, nc - jq, nbp, nbq, true, sy);
-    }
+    static const bool multi = std::getenv("QT_NO_LARFB_MULTI") == nullptr;
+    if (!multi || !larfb_multi(Vy, kp, Ty, yh + j, k, nc, nbp, static_cast<int>(p), k, sy))
+      for (long long q = 0; q < p; ++q) {
+        const long long jq = q * NB;
+        const int nbq = static_cast<int>(std::min<long long>(NB, k - jq));
+        larfb_cluster(e, Vy + jq * kp + q * NB, kp, Ty + q * NB * NB, yh + jq * k + j, k, nc - jq, nbp, nbq, true,
+                      sy);
+      }
     PanelArgs py = base;
     py.A = yh + j * k + j;
     py.lda = k;

@@ -332,3 +332,243 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
   }
   return true;
 }
+
+// Left-looking block update for the pipelined QR pair: the reflectors of
+// panels 0..nq-1 (V columns q*32.., rows q*32.. of the shared V matrix, T
+// factors T + q*32*32) applied in order to one column block A (m rows,
+// ncols <= 32 columns), A <- H_{nq-1}^H ... H_0^H A, in ONE launch.  The
+// block stays in shared memory across the nq rounds; each round stages V_q,
+// forms the partial W = V_q^H A on the FP64 tensor pipe, reduce-scatters and
+// all-gathers W through DSMEM (double-buffered inboxes and mbarriers, so no
+// cluster barrier between rounds) and applies A -= V_q (T_q^H W).
+template <int CW>
+__global__ void __launch_bounds__(LB_THREADS, 1)
+    larfb_multi_kernel(const double2* __restrict__ V, long long ldv, const double2* __restrict__ T, double2* A,
+                       long long lda, int m, int ncols, int nq, int k, int rpc) {
+  extern __shared__ __align__(16) double2 lsm[];
+  const int CS = static_cast<int>(gridDim.x);
+  const int rows_owned = (NB + CS - 1) / CS;
+  double2* Vs = lsm;                          // [rpc][32]
+  double2* As = Vs + rpc * NB;                // [rpc][CW]
+  double2* Wp = As + rpc * CW;                // [32][CW]
+  double2* Tp = Wp + NB * CW;                 // [32][32]
+  double2* Wf = Tp + NB * NB;                 // [2][32][CW]
+  double2* rs = Wf + 2 * NB * CW;             // [2][CS][rows_owned][CW]
+  __shared__ uint64_t bars[2][2];             // [round parity][reduce-scatter, all-gather]
+
+  const int tid = threadIdx.x;
+  const unsigned rank = cluster_rank();
+  const int my_rows = (NB - static_cast<int>(rank) + CS - 1) / CS;
+  const long long c0 = static_cast<long long>(blockIdx.y) * CW;
+  const int nc = static_cast<int>(min(static_cast<long long>(CW), ncols - c0));
+  const int r0 = static_cast<int>(rank) * rpc;
+  const int nloc = max(0, min(rpc, m - r0));
+  const unsigned rs_bytes = static_cast<unsigned>(CS * my_rows * CW * sizeof(double2));
+  const unsigned ag_bytes = static_cast<unsigned>(NB * CW * sizeof(double2));
+  const size_t rs_half = static_cast<size_t>(CS) * rows_owned * CW;
+
+  if (tid == 0) {
+    for (int p = 0; p < 2; ++p) {
+      pmbar_init(&bars[p][0], 1);
+      pmbar_init(&bars[p][1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int p = 0; p < 2 && p < nq; ++p) {
+      pmbar_arm(&bars[p][0], rs_bytes);
+      pmbar_arm(&bars[p][1], ag_bytes);
+    }
+  }
+  for (int e = tid; e < rpc * CW; e += LB_THREADS) {
+    const int r = e / CW, c = e % CW;
+    const bool ok = r < nloc && c < nc;
+    lb_cp16(&As[r * CW + lb_sw(r, c)], ok ? &A[static_cast<long long>(r0 + r) * lda + c0 + c] : A, ok);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  cluster_sync_all();  // barriers initialised and armed everywhere before any push
+
+  const int lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  constexpr int CB = CW / 8;
+  constexpr int OB = 4 * CB;
+  constexpr int BPW = OB >= 8 ? OB / 8 : 1;
+  constexpr int KS = OB >= 8 ? 1 : 8 / OB;
+  for (int q = 0; q < nq; ++q) {
+    const int par = q & 1;
+    const unsigned phase = static_cast<unsigned>((q >> 1) & 1);
+    const int jq = q * NB;
+    const int nbq = min(NB, k - jq);
+    if (q >= 1 && q + 1 < nq && tid == 0) {  // round q+1 reuses parity par^1: its round q-1 waits are done
+      pmbar_arm(&bars[par ^ 1][0], rs_bytes);
+      pmbar_arm(&bars[par ^ 1][1], ag_bytes);
+    }
+    // stage V_q on the local rows (zero above row jq: H_q leaves those rows alone)
+    for (int e = tid; e < rpc * NB; e += LB_THREADS) {
+      const int r = e / NB, c = e % NB;
+      const int gr = r0 + r;
+      const bool ok = r < nloc && gr >= jq;
+      lb_cp16(&Vs[r * NB + lb_sw(r, c)], ok ? &V[static_cast<long long>(gr) * ldv + jq + c] : V, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int e = tid; e < NB * NB; e += LB_THREADS) {
+      const int i = e / NB, kk = e % NB;
+      Tp[e] = (i < nbq && kk < nbq) ? cconj(T[static_cast<long long>(q) * NB * NB + kk * NB + i])
+                                    : make_double2(0.0, 0.0);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    double2* rsq = rs + par * rs_half;
+    double2* Wfq = Wf + par * NB * CW;
+    {
+      const int wb = w / KS, kh = w % KS;
+      const int rb = (wb * BPW) / CB;
+      double cre[BPW][2], cim[BPW][2];
+#pragma unroll
+      for (int b = 0; b < BPW; ++b) cre[b][0] = cre[b][1] = cim[b][0] = cim[b][1] = 0.0;
+      const int rlo = kh * (rpc / KS), rhi = rlo + rpc / KS;
+#pragma unroll 2
+      for (int r = rlo; r < rhi; r += 4) {
+        const int rr = r + t;
+        const double2 av = cconj(Vs[rr * NB + lb_sw(rr, rb * 8 + g)]);
+#pragma unroll
+        for (int b = 0; b < BPW; ++b) {
+          const int cb = (wb * BPW + b) % CB;
+          cmma(cre[b], cim[b], av, As[rr * CW + lb_sw(rr, cb * 8 + g)]);
+        }
+      }
+      if (KS > 1) {
+        if (kh == 1)
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2)
+            Wp[(rb * 8 + g) * CW + (wb % CB) * 8 + 2 * t + e2] = make_double2(cre[0][e2], cim[0][e2]);
+        __syncthreads();
+        if (kh == 0)
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const double2 o = Wp[(rb * 8 + g) * CW + (wb % CB) * 8 + 2 * t + e2];
+            cre[0][e2] += o.x;
+            cim[0][e2] += o.y;
+          }
+      }
+      if (kh == 0) {
+        const int i = rb * 8 + g;
+        const unsigned owner = static_cast<unsigned>(i % CS);
+#pragma unroll
+        for (int b = 0; b < BPW; ++b)
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int jj = ((wb * BPW + b) % CB) * 8 + 2 * t + e2;
+            double2* slot = &rsq[(static_cast<int>(rank) * rows_owned + i / CS) * CW + jj];
+            st_async_push(cl_map(slot, owner), make_double2(cre[b][e2], cim[b][e2]), cl_map(&bars[par][0], owner));
+          }
+      }
+    }
+    pmbar_wait(&bars[par][0], phase);
+    {
+      const int nent = my_rows * CW;
+      const int groups = max(1, min(CS, LB_THREADS / max(1, nent)));
+      for (int e = tid; e < nent * groups; e += LB_THREADS) {
+        const int ent = e / groups, gg = e % groups;
+        const int li = ent / CW, jj = ent % CW;
+        const int i = static_cast<int>(rank) + li * CS;
+        double2 s = make_double2(0.0, 0.0);
+        for (int src = 0; src < CS; ++src) s = cadd(s, rsq[(src * rows_owned + li) * CW + jj]);
+        for (int dst = gg; dst < CS; dst += groups)
+          st_async_push(cl_map(&Wfq[i * CW + jj], dst), s, cl_map(&bars[par][1], dst));
+      }
+    }
+    pmbar_wait(&bars[par][1], phase);
+    if (w < OB / BPW) {  // W2 = T_q^H W
+      const int rb = (w * BPW) / CB;
+      double cre[BPW][2], cim[BPW][2];
+#pragma unroll
+      for (int b = 0; b < BPW; ++b) cre[b][0] = cre[b][1] = cim[b][0] = cim[b][1] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const double2 av = Tp[(rb * 8 + g) * NB + k0 + t];
+#pragma unroll
+        for (int b = 0; b < BPW; ++b) {
+          const int cb = (w * BPW + b) % CB;
+          cmma(cre[b], cim[b], av, Wfq[(k0 + t) * CW + cb * 8 + g]);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < BPW; ++b)
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2)
+          Wp[(rb * 8 + g) * CW + ((w * BPW + b) % CB) * 8 + 2 * t + e2] = make_double2(cre[b][e2], cim[b][e2]);
+    }
+    __syncthreads();
+    // A_r -= V_q W2 in shared memory
+    for (int blk = w; blk < (rpc / 8) * CB; blk += LB_THREADS / 32) {
+      const int rb = blk / CB, cb = blk % CB, row = rb * 8 + g;
+      double cre[2], cim[2];
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const double2 c = As[row * CW + lb_sw(row, cb * 8 + 2 * t + e2)];
+        cre[e2] = c.x;
+        cim[e2] = c.y;
+      }
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const double2 av = Vs[row * NB + lb_sw(row, k0 + t)];
+        cmma(cre, cim, make_double2(-av.x, -av.y), Wp[(k0 + t) * CW + cb * 8 + g]);
+      }
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) As[row * CW + lb_sw(row, cb * 8 + 2 * t + e2)] = make_double2(cre[e2], cim[e2]);
+    }
+    __syncthreads();  // A updated before the next round's partials; Vs/Tp/Wp free for restaging
+  }
+  for (int e = tid; e < nloc * CW; e += LB_THREADS) {
+    const int r = e / CW, c = e % CW;
+    if (c < nc) A[static_cast<long long>(r0 + r) * lda + c0 + c] = As[r * CW + lb_sw(r, c)];
+  }
+  cluster_sync_all();  // no CTA retires while a peer may still push into it
+}
+
+constexpr size_t larfb_multi_smem(int rpc, int cs, int cw) {
+  return (size_t(rpc) * (NB + cw) + NB * cw + NB * NB + 2 * NB * cw + 2 * size_t(cs) * ((NB + cs - 1) / cs) * cw) *
+         sizeof(double2);
+}
+
+template <int CW>
+void larfb_multi_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv, const double2* T, double2* A,
+                        long long lda, long long m, long long ncols, int nq, long long k, long long rpc) {
+  static bool attr = false;
+  if (!attr) {
+    QT_CUDA(cudaFuncSetAttribute(larfb_multi_kernel<CW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    QT_CUDA(cudaFuncSetAttribute(larfb_multi_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(larfb_multi_smem(LB_MAX_RPC, 16, 32))));
+    attr = true;
+  }
+  QT_CUDA(cudaLaunchKernelEx(&cfg, larfb_multi_kernel<CW>, V, ldv, T, A, lda, static_cast<int>(m),
+                             static_cast<int>(ncols), nq, static_cast<int>(k), static_cast<int>(rpc)));
+}
+
+// A (m x ncols <= 32, ld lda) <- H_{nq-1}^H ... H_0^H A with the reflectors of
+// panels 0..nq-1 stored in V (ld ldv; panel q in columns q*32.., from row q*32)
+// and T (32 x 32 per panel) of a k-column QR; false when m is too tall
+bool larfb_multi(const double2* V, long long ldv, const double2* T, double2* A, long long lda, long long m,
+                 long long ncols, int nq, long long k, cudaStream_t st) {
+  const int max_cs = larfb_max_cs();
+  if (max_cs == 0 || ncols <= 0 || ncols > NB) return false;
+  if (nq <= 0) return true;
+  long long rpc = std::max<long long>(8, ceil_div(m, max_cs));
+  rpc = ceil_div(rpc, 8) * 8;
+  if (rpc > LB_MAX_RPC) return false;
+  const long long cs = ceil_div(m, rpc);
+  const int cw = 8;  // four clusters of 8 columns: more SMs on the chain
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(ceil_div(ncols, cw)));
+  cfg.blockDim = dim3(LB_THREADS);
+  cfg.dynamicSmemBytes = larfb_multi_smem(static_cast<int>(rpc), static_cast<int>(cs), cw);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = static_cast<unsigned>(cs);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  larfb_multi_launch<8>(cfg, V, ldv, T, A, lda, m, ncols, nq, k, rpc);
+  QT_LAUNCHED();
+  return true;
+}
