@@ -36,6 +36,7 @@ void Engine::init(int dev, cudaStream_t st) {
   QT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   QT_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   QT_CUDA(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, no_prio ? prio_least : prio_greatest));
+  QT_CUDA(cudaStreamCreateWithFlags(&side4, cudaStreamNonBlocking));
 }
 
 cudaEvent_t Engine::event(size_t i) {
@@ -72,6 +73,11 @@ void Engine::destroy() {
     cudaStreamDestroy(side3);
   }
   side3 = nullptr;
+  if (side4) {
+    cudaStreamSynchronize(side4);
+    cudaStreamDestroy(side4);
+  }
+  side4 = nullptr;
   for (cudaEvent_t ev : events) cudaEventDestroy(ev);
   events.clear();
   dscal = nullptr;

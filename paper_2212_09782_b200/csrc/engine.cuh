@@ -79,6 +79,9 @@ struct Engine {
   cudaStream_t side2 = nullptr;
   // fourth stream: the second QR of a pipelined pair (qr_pair_pipelined)
   cudaStream_t side3 = nullptr;
+  // fifth stream: column blocks of the pair's explicit Q, formed as soon as
+  // their reflectors exist
+  cudaStream_t side4 = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t event(size_t i);
 

@@ -206,10 +206,16 @@ void gemm(Engine& e, Op oa, Op ob, long long M, long long N, long long K, const 
 }  // namespace
 
 bool use_qtheta(const qt_policy& pol, long long rows) {
+  // above ~2048 rows the extra reflector flops on theta outweigh the shorter
+  // critical path (north star: GEMM-bound); below ~256 the side-stream
+  // launches cost more than they hide (C5-small: 8 concurrent bonds)
   static const long long qtheta_max = std::getenv("QT_QTHETA_MAX_ROWS")
                                           ? std::atoll(std::getenv("QT_QTHETA_MAX_ROWS"))
                                           : 2048;
-  return std::max(1, static_cast<int>(pol.qr_sweeps)) == 1 && rows <= qtheta_max;
+  static const long long qtheta_min = std::getenv("QT_QTHETA_MIN_ROWS")
+                                          ? std::atoll(std::getenv("QT_QTHETA_MIN_ROWS"))
+                                          : 256;
+  return std::max(1, static_cast<int>(pol.qr_sweeps)) == 1 && rows <= qtheta_max && rows >= qtheta_min;
 }
 
 void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh,

@@ -603,6 +603,15 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
   // the Y chain may only start after everything earlier on the caller's stream
   QT_CUDA(cudaEventRecord(e.event(J0), sx));
   QT_CUDA(cudaStreamWaitEvent(sy, e.event(J0), 0));
+  // explicit Q of Y^H formed block by block on sq behind the Y chain: column
+  // block b of Q = H'_0 ... H'_b [e_{32b} .. e_{32b+31}] (reflectors > b leave
+  // those columns alone), one reverse multi-reflector launch per block
+  static const bool qblocks = std::getenv("QT_NO_QBLOCKS") == nullptr;
+  const cudaStream_t sq = e.side4;
+  const size_t Q0 = J0 + 8;  // events: Y panel b done
+  if (qblocks) {
+    set_identity(e, qy, nc, k, k, sy);
+  }
 
   bool wide_pending = false;
   long long last_wide = -1;
@@ -661,19 +670,30 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     py.ldv = kp;
     py.T = Ty + p * NB * NB;
     launch_panel(e, py, nc - j, sy);
+    if (qblocks) {
+      QT_CUDA(cudaEventRecord(e.event(Q0 + p), sy));
+      QT_CUDA(cudaStreamWaitEvent(sq, e.event(Q0 + p), 0));
+      if (!larfb_multi(Vy, kp, Ty, qy + j, k, nc, nbp, static_cast<int>(p + 1), k, sq, true, false))
+        throw Error(Err::internal, "qr_pair_pipelined: Q block does not fit a cluster");
+    }
   }
   // join the X side streams (R of X is not needed; its diagonal carries the gauge phases)
   if (last_wide >= 0) QT_CUDA(cudaStreamWaitEvent(sx, e.event(2 * last_wide + 1), 0));
   QT_CUDA(cudaEventRecord(e.event(J0 + 1), sa));
   QT_CUDA(cudaStreamWaitEvent(sx, e.event(J0 + 1), 0));
-  // explicit thin Q of Y^H = H'_0 ... H'_{k-1} I[:, :k] (backward block reflectors) on sy
-  set_identity(e, qy, nc, k, k, sy);
-  for (long long p = npan - 1; p >= 0; --p) {
-    const long long j = p * NB;
-    const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
-    if (!larfb_cluster(e, Vy + j * kp + p * NB, kp, Ty + p * NB * NB, qy + j * k + j, k, nc - j, k - j, nbp, false,
-                       sy))
-      throw Error(Err::internal, "qr_pair_pipelined: block reflector does not fit a cluster");
+  if (qblocks) {  // join sq: every column block of Q formed
+    QT_CUDA(cudaEventRecord(e.event(Q0 + npan), sq));
+    QT_CUDA(cudaStreamWaitEvent(sy, e.event(Q0 + npan), 0));
+  } else {
+    // explicit thin Q of Y^H = H'_0 ... H'_{k-1} I[:, :k] (backward block reflectors) on sy
+    set_identity(e, qy, nc, k, k, sy);
+    for (long long p = npan - 1; p >= 0; --p) {
+      const long long j = p * NB;
+      const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+      if (!larfb_cluster(e, Vy + j * kp + p * NB, kp, Ty + p * NB * NB, qy + j * k + j, k, nc - j, k - j, nbp,
+                         false, sy))
+        throw Error(Err::internal, "qr_pair_pipelined: block reflector does not fit a cluster");
+    }
   }
   gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
   QT_LAUNCHED();

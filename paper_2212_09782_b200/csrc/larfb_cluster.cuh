@@ -333,7 +333,8 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
   return true;
 }
 
-// Left-looking block update for the pipelined QR pair: the reflectors of
+// Left-looking block update for the pipelined QR pair (and, in reverse with
+// T instead of T^H, one column block of the explicit Q): the reflectors of
 // panels 0..nq-1 (V columns q*32.., rows q*32.. of the shared V matrix, T
 // factors T + q*32*32) applied in order to one column block A (m rows,
 // ncols <= 32 columns), A <- H_{nq-1}^H ... H_0^H A, in ONE launch.  The
@@ -344,7 +345,7 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
 template <int CW>
 __global__ void __launch_bounds__(LB_THREADS, 1)
     larfb_multi_kernel(const double2* __restrict__ V, long long ldv, const double2* __restrict__ T, double2* A,
-                       long long lda, int m, int ncols, int nq, int k, int rpc) {
+                       long long lda, int m, int ncols, int nq, int k, int rpc, int reverse, int use_th) {
   extern __shared__ __align__(16) double2 lsm[];
   const int CS = static_cast<int>(gridDim.x);
   const int rows_owned = (NB + CS - 1) / CS;
@@ -391,12 +392,13 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   constexpr int OB = 4 * CB;
   constexpr int BPW = OB >= 8 ? OB / 8 : 1;
   constexpr int KS = OB >= 8 ? 1 : 8 / OB;
-  for (int q = 0; q < nq; ++q) {
-    const int par = q & 1;
-    const unsigned phase = static_cast<unsigned>((q >> 1) & 1);
+  for (int it = 0; it < nq; ++it) {
+    const int par = it & 1;
+    const unsigned phase = static_cast<unsigned>((it >> 1) & 1);
+    const int q = reverse ? nq - 1 - it : it;  // reverse: H_{nq-1} first (explicit Q, zungqr order)
     const int jq = q * NB;
     const int nbq = min(NB, k - jq);
-    if (q >= 1 && q + 1 < nq && tid == 0) {  // round q+1 reuses parity par^1: its round q-1 waits are done
+    if (it >= 1 && it + 1 < nq && tid == 0) {  // round it+1 reuses parity par^1: its round it-1 waits are done
       pmbar_arm(&bars[par ^ 1][0], rs_bytes);
       pmbar_arm(&bars[par ^ 1][1], ag_bytes);
     }
@@ -410,8 +412,8 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
     asm volatile("cp.async.commit_group;" ::: "memory");
     for (int e = tid; e < NB * NB; e += LB_THREADS) {
       const int i = e / NB, kk = e % NB;
-      Tp[e] = (i < nbq && kk < nbq) ? cconj(T[static_cast<long long>(q) * NB * NB + kk * NB + i])
-                                    : make_double2(0.0, 0.0);
+      const double2* Tq = T + static_cast<long long>(q) * NB * NB;
+      Tp[e] = (i < nbq && kk < nbq) ? (use_th ? cconj(Tq[kk * NB + i]) : Tq[i * NB + kk]) : make_double2(0.0, 0.0);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
@@ -531,7 +533,8 @@ constexpr size_t larfb_multi_smem(int rpc, int cs, int cw) {
 
 template <int CW>
 void larfb_multi_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv, const double2* T, double2* A,
-                        long long lda, long long m, long long ncols, int nq, long long k, long long rpc) {
+                        long long lda, long long m, long long ncols, int nq, long long k, long long rpc, bool reverse,
+                        bool use_th) {
   static bool attr = false;
   if (!attr) {
     QT_CUDA(cudaFuncSetAttribute(larfb_multi_kernel<CW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -540,14 +543,16 @@ void larfb_multi_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv
     attr = true;
   }
   QT_CUDA(cudaLaunchKernelEx(&cfg, larfb_multi_kernel<CW>, V, ldv, T, A, lda, static_cast<int>(m),
-                             static_cast<int>(ncols), nq, static_cast<int>(k), static_cast<int>(rpc)));
+                             static_cast<int>(ncols), nq, static_cast<int>(k), static_cast<int>(rpc), reverse ? 1 : 0,
+                             use_th ? 1 : 0));
 }
 
 // A (m x ncols <= 32, ld lda) <- H_{nq-1}^H ... H_0^H A with the reflectors of
 // panels 0..nq-1 stored in V (ld ldv; panel q in columns q*32.., from row q*32)
 // and T (32 x 32 per panel) of a k-column QR; false when m is too tall
+// (reverse = true, use_th = false: A <- H_0 ... H_{nq-1} A, the explicit-Q order)
 bool larfb_multi(const double2* V, long long ldv, const double2* T, double2* A, long long lda, long long m,
-                 long long ncols, int nq, long long k, cudaStream_t st) {
+                 long long ncols, int nq, long long k, cudaStream_t st, bool reverse = false, bool use_th = true) {
   const int max_cs = larfb_max_cs();
   if (max_cs == 0 || ncols <= 0 || ncols > NB) return false;
   if (nq <= 0) return true;
@@ -568,7 +573,7 @@ bool larfb_multi(const double2* V, long long ldv, const double2* T, double2* A, 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  larfb_multi_launch<8>(cfg, V, ldv, T, A, lda, m, ncols, nq, k, rpc);
+  larfb_multi_launch<8>(cfg, V, ldv, T, A, lda, m, ncols, nq, k, rpc, reverse, use_th);
   QT_LAUNCHED();
   return true;
 }
