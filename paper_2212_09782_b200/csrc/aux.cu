@@ -37,6 +37,7 @@ void Engine::init(int dev, cudaStream_t st) {
   QT_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   QT_CUDA(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, no_prio ? prio_least : prio_greatest));
   QT_CUDA(cudaStreamCreateWithFlags(&side4, cudaStreamNonBlocking));
+  QT_CUDA(cudaStreamCreateWithFlags(&side5, cudaStreamNonBlocking));
 }
 
 cudaEvent_t Engine::event(size_t i) {
@@ -78,6 +79,11 @@ void Engine::destroy() {
     cudaStreamDestroy(side4);
   }
   side4 = nullptr;
+  if (side5) {
+    cudaStreamSynchronize(side5);
+    cudaStreamDestroy(side5);
+  }
+  side5 = nullptr;
   for (cudaEvent_t ev : events) cudaEventDestroy(ev);
   events.clear();
   dscal = nullptr;

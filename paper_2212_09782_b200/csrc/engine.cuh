@@ -82,6 +82,9 @@ struct Engine {
   // fifth stream: column blocks of the pair's explicit Q, formed as soon as
   // their reflectors exist
   cudaStream_t side4 = nullptr;
+  // sixth stream: left-looking updates of the pair's Y^H blocks, concurrent
+  // with the Y panel before them
+  cudaStream_t side5 = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t event(size_t i);
 

@@ -20,6 +20,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "engine.cuh"
 
@@ -607,12 +609,28 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
   // block b of Q = H'_0 ... H'_b [e_{32b} .. e_{32b+31}] (reflectors > b leave
   // those columns alone), one reverse multi-reflector launch per block
   static const bool qblocks = std::getenv("QT_NO_QBLOCKS") == nullptr;
-  const cudaStream_t sq = e.side4;
-  const size_t Q0 = J0 + 8;  // events: Y panel b done
+  const cudaStream_t sq = e.side4, su = e.side5;
+  const size_t Q0 = J0 + 8;         // events: Y panel b done
+  const size_t U0 = Q0 + npan + 2;  // events: block p updated with reflectors 0..p-2
   if (qblocks) {
     set_identity(e, qy, nc, k, k, sy);
   }
 
+  // QT_PAIR_DEBUG=1 (eager calls only): timeline of the pair on stderr
+  static const bool tdbg = std::getenv("QT_PAIR_DEBUG") != nullptr;
+  static std::vector<cudaEvent_t> tev;
+  std::vector<std::string> tname;
+  auto stamp = [&](const std::string& nm, cudaStream_t st) {
+    if (!tdbg) return;
+    if (tev.size() <= tname.size()) {
+      cudaEvent_t ev;
+      QT_CUDA(cudaEventCreate(&ev));
+      tev.push_back(ev);
+    }
+    QT_CUDA(cudaEventRecord(tev[tname.size()], st));
+    tname.push_back(nm);
+  };
+  stamp("start", sx);
   bool wide_pending = false;
   long long last_wide = -1;
   for (long long p = 0; p < npan; ++p) {
@@ -628,11 +646,13 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     pa.ldv = kp;
     pa.T = Tx + p * NB * NB;
     launch_panel(e, pa, m - j, sx);
+    stamp("Xpanel" + std::to_string(p), sx);
     // ---- theta side: C <- H_p^H C, then rows [j, j + nbp) of C are final
     QT_CUDA(cudaEventRecord(e.event(P0 + p), sx));
     QT_CUDA(cudaStreamWaitEvent(sa, e.event(P0 + p), 0));
     apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa);
     extract(j, nbp, sa);
+    stamp("extract" + std::to_string(p), sa);
     QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
     // ---- X trailing update (look-ahead: next panel's columns on sx, the rest on sxw)
     const long long ntr = k - j - nbp;
@@ -644,23 +664,35 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
         QT_CUDA(cudaStreamWaitEvent(sxw, e.event(2 * p), 0));
       }
       larfb_cluster(e, pa.V, kp, pa.T, x + j * k + j + nbp, k, m - j, nn, nbp, true, sx);
+      stamp("Xnarrow" + std::to_string(p), sx);
       wide_pending = ntr > nn;
       if (wide_pending) {
         larfb_cluster(e, pa.V, kp, pa.T, x + j * k + j + nbp + nn, k, m - j, ntr - nn, nbp, true, sxw);
+        stamp("Xwide" + std::to_string(p), sxw);
         QT_CUDA(cudaEventRecord(e.event(2 * p + 1), sxw));
         last_wide = p;
       }
     }
     // ---- Y^H: block p receives the reflectors of Y panels < p, then panel p
-    QT_CUDA(cudaStreamWaitEvent(sy, e.event(E0 + p), 0));
-    static const bool multi = std::getenv("QT_NO_LARFB_MULTI") == nullptr;
-    if (!multi || !larfb_multi(Vy, kp, Ty, yh + j, k, nc, nbp, static_cast<int>(p), k, sy))
-      for (long long q = 0; q < p; ++q) {
-        const long long jq = q * NB;
-        const int nbq = static_cast<int>(std::min<long long>(NB, k - jq));
-        larfb_cluster(e, Vy + jq * kp + q * NB, kp, Ty + q * NB * NB, yh + jq * k + j, k, nc - jq, nbp, nbq, true,
-                      sy);
-      }
+    // block p receives reflectors 0..p-2 on su (concurrently with Y panel
+    // p-1, once that panel's predecessor exists), then H'_{p-1} on sy right
+    // after Y panel p-1: the Y chain carries only narrow updates
+    if (p >= 2) {
+      QT_CUDA(cudaStreamWaitEvent(su, e.event(E0 + p), 0));
+      QT_CUDA(cudaStreamWaitEvent(su, e.event(Q0 + p - 2), 0));
+      if (!larfb_multi(Vy, kp, Ty, yh + j, k, nc, nbp, static_cast<int>(p - 1), k, su))
+        throw Error(Err::internal, "qr_pair_pipelined: block update does not fit a cluster");
+      QT_CUDA(cudaEventRecord(e.event(U0 + p), su));
+      QT_CUDA(cudaStreamWaitEvent(sy, e.event(U0 + p), 0));
+    } else {
+      QT_CUDA(cudaStreamWaitEvent(sy, e.event(E0 + p), 0));
+    }
+    stamp("Ystart" + std::to_string(p), sy);
+    if (p >= 1) {
+      const long long jq = (p - 1) * NB;
+      larfb_cluster(e, Vy + jq * kp + (p - 1) * NB, kp, Ty + (p - 1) * NB * NB, yh + jq * k + j, k, nc - jq, nbp, NB,
+                    true, sy);
+    }
     PanelArgs py = base;
     py.A = yh + j * k + j;
     py.lda = k;
@@ -669,12 +701,15 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     py.V = Vy + j * kp + p * NB;
     py.ldv = kp;
     py.T = Ty + p * NB * NB;
+    stamp("Yupdate" + std::to_string(p), sy);
     launch_panel(e, py, nc - j, sy);
+    stamp("Ypanel" + std::to_string(p), sy);
+    QT_CUDA(cudaEventRecord(e.event(Q0 + p), sy));  // Y panel p done: V'_p, T'_p exist
     if (qblocks) {
-      QT_CUDA(cudaEventRecord(e.event(Q0 + p), sy));
       QT_CUDA(cudaStreamWaitEvent(sq, e.event(Q0 + p), 0));
       if (!larfb_multi(Vy, kp, Ty, qy + j, k, nc, nbp, static_cast<int>(p + 1), k, sq, true, false))
         throw Error(Err::internal, "qr_pair_pipelined: Q block does not fit a cluster");
+      stamp("Qblock" + std::to_string(p), sq);
     }
   }
   // join the X side streams (R of X is not needed; its diagonal carries the gauge phases)
@@ -701,6 +736,17 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
   QT_LAUNCHED();
   QT_CUDA(cudaEventRecord(e.event(J0 + 2), sy));
   QT_CUDA(cudaStreamWaitEvent(sx, e.event(J0 + 2), 0));
+  stamp("end", sx);
+  if (tdbg) {
+    QT_CUDA(cudaStreamSynchronize(sx));
+    std::fprintf(stderr, "qr_pair m=%lld k=%lld nc=%lld timeline (us from start):", m, k, nc);
+    for (size_t i = 1; i < tname.size(); ++i) {
+      float ms = 0.f;
+      QT_CUDA(cudaEventElapsedTime(&ms, tev[0], tev[i]));
+      std::fprintf(stderr, " %s=%.0f", tname[i].c_str(), ms * 1000.f);
+    }
+    std::fprintf(stderr, "\n");
+  }
 }
 
 }  // namespace qt
