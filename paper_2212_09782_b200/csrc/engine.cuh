@@ -45,6 +45,8 @@ enum Slot : int {
   S_QT_PART,     // partial sums of the Q^H theta residual
   S_QR_V2,       // reflectors / T factors of the second QR of a pipelined pair
   S_QR_T2,
+  S_GEMM_PART3,  // split-K scratch of GEMMs on side4 (consumers of the pair's Q blocks)
+  S_TILE_SUMS3,
   S_COUNT
 };
 
@@ -96,6 +98,7 @@ struct Engine {
   double* dbuf(int slot, size_t elems) { return static_cast<double*>(raw(slot, elems * sizeof(double))); }
   GemmScratch gemm_scratch();
   GemmScratch gemm_scratch2();  // separate split-K buffers for GEMMs on side2
+  GemmScratch gemm_scratch3();  // ... and on side4
 };
 
 // ---- kernels shared by the modules (aux.cu) -------------------------------
@@ -140,8 +143,11 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 // heights within one block-reflector cluster (qr_pair_fits).  Everything is
 // joined into e.stream on return.
 bool qr_pair_fits(long long m, long long nc);
+// on_qblock (optional): called on the Q stream once columns [c0, c0 + nb) of
+// qy are formed and gauge-fixed (consumers of Q start behind the Y chain).
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
                        double2* qy, double2* ry,
-                       const std::function<void(long long, long long, cudaStream_t)>& extract);
+                       const std::function<void(long long, long long, cudaStream_t)>& extract,
+                       const std::function<void(long long, long long, cudaStream_t)>& on_qblock = nullptr);
 
 }  // namespace qt

@@ -307,6 +307,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   // is wanted), no theta^H Q_m GEMM, and the explicit error needs only
   // ||Y - L Q_n||^2 + ||Z||^2 instead of a theta-sized residual product
   const bool qtheta = use_qtheta(pol, rows);
+  bool hastings_done = false;
   for (int it = 0; it < sweeps; ++it) {
     if (it == 0)
       gemm(e, Op::N, Op::H, rows, eta, cols, theta, cols, y0, cols, X, eta);  // X = theta Y0^H
@@ -315,10 +316,24 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
     if (qtheta && !out.left_iso && use_qr_pair(rows, cols)) {
       // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
-      qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp,
-                        [&](long long r0, long long nr, cudaStream_t st) {
-                          qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st);
-                        });
+      // the Hastings columns of B~m follow the Q blocks of Y^H: column block b
+      // of B~m = phiev Qp[:, b] as soon as that block of Qp exists
+      const GemmScratch gs3 = e.gemm_scratch3();
+      std::function<void(long long, long long, cudaStream_t)> hastings_block;
+      if (out.b_m)
+        hastings_block = [&](long long c0, long long nb, cudaStream_t st) {
+          GemmDesc g;
+          g.M = cm * d; g.N = nb; g.K = cols;
+          g.A = phiev; g.lda = cols;
+          g.B = Qp + c0; g.ldb = eta;
+          g.C = out.b_m + c0; g.ldc = cm * eta; g.rsplit = d; g.ldc_hi = eta;
+          zgemm(g, gs3, st);
+        };
+      qr_pair_pipelined(
+          e, X, rows, eta, theta, cols, YH, Qp, Rp,
+          [&](long long r0, long long nr, cudaStream_t st) { qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st); },
+          hastings_block);
+      hastings_done = true;
       check_finite(e, theta, eta * cols, flag);  // Y (the first eta rows of Q_full^H theta)
       continue;
     }
@@ -353,7 +368,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     const int perm[3] = {0, 2, 1};
     permute(e, Qp, 3, shp, perm, true, out.b_n);
   }
-  if (out.b_m) {
+  if (out.b_m && !hastings_done) {
     // B~m[i,beta,k] = sum_{j,delta} phiev[beta,i,j,delta] conj(B~n[j,k,delta])
     //             = (phiev (cm*d x d*cr) . Qp)[(beta i), k]   (gates.cpp:186-190)
     // (skipped when the caller keeps left_iso instead: the reference finite

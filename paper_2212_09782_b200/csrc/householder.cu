@@ -222,6 +222,20 @@ __global__ void gauge_q_kernel(const double2* __restrict__ a, long long lda, dou
   }
 }
 
+// gauge phases on columns [c0, c0 + nb) of q only (one Q block of the pair)
+__global__ void gauge_q_cols_kernel(const double2* __restrict__ a, long long lda, double2* q, long long ldq,
+                                    long long m, long long c0, long long nb) {
+  const long long total = m * nb;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = e / nb, c = c0 + e % nb;
+    const double2 d = a[c * lda + c];
+    const double ad = hypot(d.x, d.y);
+    if (ad == 0.0) continue;
+    q[r * ldq + c] = cmul(q[r * ldq + c], make_double2(d.x / ad, d.y / ad));
+  }
+}
+
 __global__ void gauge_r_kernel(const double2* __restrict__ a, long long lda, double2* r, long long ldr,
                                long long k, long long n) {
   const long long total = k * n;
@@ -578,7 +592,8 @@ bool qr_pair_fits(long long m, long long nc) { return larfb_cluster_fits(m) && l
 
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
                        double2* qy, double2* ry,
-                       const std::function<void(long long, long long, cudaStream_t)>& extract) {
+                       const std::function<void(long long, long long, cudaStream_t)>& extract,
+                       const std::function<void(long long, long long, cudaStream_t)>& on_qblock) {
   if (k == 0) return;
   if (k > m || k > nc || !qr_pair_fits(m, nc)) throw Error(Err::internal, "qr_pair_pipelined: shape not supported");
   const long long npan = ceil_div(k, NB);
@@ -709,6 +724,10 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
       QT_CUDA(cudaStreamWaitEvent(sq, e.event(Q0 + p), 0));
       if (!larfb_multi(Vy, kp, Ty, qy + j, k, nc, nbp, static_cast<int>(p + 1), k, sq, true, false))
         throw Error(Err::internal, "qr_pair_pipelined: Q block does not fit a cluster");
+      // gauge the block now (the phases of its R' diagonal are final after Y panel p)
+      gauge_q_cols_kernel<<<grid_for(nc * nbp), 256, 0, sq>>>(yh, k, qy, k, nc, j, nbp);
+      QT_LAUNCHED();
+      if (on_qblock) on_qblock(j, nbp, sq);
       stamp("Qblock" + std::to_string(p), sq);
     }
   }
@@ -730,8 +749,11 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
         throw Error(Err::internal, "qr_pair_pipelined: block reflector does not fit a cluster");
     }
   }
-  gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
-  QT_LAUNCHED();
+  if (!qblocks) {
+    gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
+    QT_LAUNCHED();
+    if (on_qblock) on_qblock(0, k, sy);
+  }
   gauge_r_kernel<<<grid_for(k * k), 256, 0, sy>>>(yh, k, ry, k, k, k);
   QT_LAUNCHED();
   QT_CUDA(cudaEventRecord(e.event(J0 + 2), sy));

@@ -31,4 +31,8 @@ full jacobi_c2cbe jacobi_kernel 1 python tools/eigh_one.py 356
 full larfb32_c2 larfb_cluster 0 python tools/qr_one.py 1280 256 2  # first launch: trailing update, cw = 32
 full permute_c2 permute_kernel 2 python tools/profile_step.py --config c2
 full transpose_c2 transpose_tiled_kernel 1 python tools/profile_step.py --config c2
+# pipelined QR pair (C2 step): multi-reflector block update, Y^H extraction, Q^H theta residual
+full larfbmulti_c2 larfb_multi_kernel 6 python tools/profile_step.py --config c2
+full yhgauge_c2 yh_gauge_kernel 3 python tools/profile_step.py --config c2
+full qtresid_c2 qtheta_resid_partial_kernel 1 python tools/profile_step.py --config c2
 tail -1 $P/ncu_*.log
