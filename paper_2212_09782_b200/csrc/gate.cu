@@ -316,11 +316,14 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
     if (qtheta && !out.left_iso && use_qr_pair(rows, cols)) {
       // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
-      // the Hastings columns of B~m follow the Q blocks of Y^H: column block b
-      // of B~m = phiev Qp[:, b] as soon as that block of Qp exists
+      // QT_QB_HASTINGS=1: the Hastings columns of B~m follow the Q blocks of
+      // Y^H (column block b of B~m = phiev Qp[:, b] as soon as that block of Qp
+      // exists); measured slower at C2 (172 vs 181 steps/s: the per-block
+      // GEMMs contend with both panel chains), so off by default
       const GemmScratch gs3 = e.gemm_scratch3();
       std::function<void(long long, long long, cudaStream_t)> hastings_block;
-      if (out.b_m)
+      static const bool qb_hastings = std::getenv("QT_QB_HASTINGS") != nullptr;
+      if (out.b_m && qb_hastings)
         hastings_block = [&](long long c0, long long nb, cudaStream_t st) {
           GemmDesc g;
           g.M = cm * d; g.N = nb; g.K = cols;
@@ -333,7 +336,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
           e, X, rows, eta, theta, cols, YH, Qp, Rp,
           [&](long long r0, long long nr, cudaStream_t st) { qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st); },
           hastings_block);
-      hastings_done = true;
+      hastings_done = static_cast<bool>(hastings_block);
       check_finite(e, theta, eta * cols, flag);  // Y (the first eta rows of Q_full^H theta)
       continue;
     }
