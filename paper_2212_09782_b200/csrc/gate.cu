@@ -88,16 +88,27 @@ __global__ void yh_gauge_kernel(const double2* __restrict__ qt, long long cols, 
 __global__ void qtheta_resid_partial_kernel(const double2* __restrict__ qt, long long rows, long long cols,
                                             const double2* __restrict__ a, long long lda, long long eta,
                                             const double2* __restrict__ w, double* part) {
+  // block b owns rows b, b + gridDim.x, ...: one phase per row, coalesced
+  // column sweeps, two accumulation chains; fixed order -> deterministic
   __shared__ double sh[256];
-  double s = 0.0;
-  const long long total = rows * cols;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long i = e / cols;
-    double2 v = qt[e];
-    if (i < eta) v = csub(cmul(cconj(qr_phase(a, lda, i)), v), w[e]);
-    s = fma(v.x, v.x, fma(v.y, v.y, s));
+  double s = 0.0, s1 = 0.0;
+  for (long long i = blockIdx.x; i < rows; i += gridDim.x) {
+    const double2* row = qt + i * cols;
+    if (i < eta) {
+      const double2 ph = cconj(qr_phase(a, lda, i));
+      const double2* wr = w + i * cols;
+      for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+        const double2 v = csub(cmul(ph, row[c]), wr[c]);
+        s = fma(v.x, v.x, fma(v.y, v.y, s));
+      }
+    } else {
+      for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
+        const double2 v = row[c];
+        s1 = fma(v.x, v.x, fma(v.y, v.y, s1));
+      }
+    }
   }
+  s += s1;
   sh[threadIdx.x] = s;
   __syncthreads();
   for (int k = blockDim.x / 2; k > 0; k >>= 1) {

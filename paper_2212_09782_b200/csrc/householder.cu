@@ -722,11 +722,9 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     QT_CUDA(cudaEventRecord(e.event(Q0 + p), sy));  // Y panel p done: V'_p, T'_p exist
     if (qblocks) {
       QT_CUDA(cudaStreamWaitEvent(sq, e.event(Q0 + p), 0));
-      if (!larfb_multi(Vy, kp, Ty, qy + j, k, nc, nbp, static_cast<int>(p + 1), k, sq, true, false))
+      // gauge-fixed on write-back (the phases of its R' diagonal are final after Y panel p)
+      if (!larfb_multi(Vy, kp, Ty, qy + j, k, nc, nbp, static_cast<int>(p + 1), k, sq, true, false, yh, k, j))
         throw Error(Err::internal, "qr_pair_pipelined: Q block does not fit a cluster");
-      // gauge the block now (the phases of its R' diagonal are final after Y panel p)
-      gauge_q_cols_kernel<<<grid_for(nc * nbp), 256, 0, sq>>>(yh, k, qy, k, nc, j, nbp);
-      QT_LAUNCHED();
       if (on_qblock) on_qblock(j, nbp, sq);
       stamp("Qblock" + std::to_string(p), sq);
     }

@@ -345,7 +345,8 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
 template <int CW>
 __global__ void __launch_bounds__(LB_THREADS, 1)
     larfb_multi_kernel(const double2* __restrict__ V, long long ldv, const double2* __restrict__ T, double2* A,
-                       long long lda, int m, int ncols, int nq, int k, int rpc, int reverse, int use_th) {
+                       long long lda, int m, int ncols, int nq, int k, int rpc, int reverse, int use_th,
+                       const double2* __restrict__ ph, long long ph_ld, long long ph_col0) {
   extern __shared__ __align__(16) double2 lsm[];
   const int CS = static_cast<int>(gridDim.x);
   const int rows_owned = (NB + CS - 1) / CS;
@@ -521,7 +522,15 @@ __global__ void __launch_bounds__(LB_THREADS, 1)
   }
   for (int e = tid; e < nloc * CW; e += LB_THREADS) {
     const int r = e / CW, c = e % CW;
-    if (c < nc) A[static_cast<long long>(r0 + r) * lda + c0 + c] = As[r * CW + lb_sw(r, c)];
+    if (c >= nc) continue;
+    double2 v = As[r * CW + lb_sw(r, c)];
+    if (ph) {  // gauge phase R_cc / |R_cc| of global column gc (explicit Q, linalg.cpp:25-36)
+      const long long gc = ph_col0 + c0 + c;
+      const double2 d = ph[gc * ph_ld + gc];
+      const double ad = hypot(d.x, d.y);
+      if (ad != 0.0) v = cmul(v, make_double2(d.x / ad, d.y / ad));
+    }
+    A[static_cast<long long>(r0 + r) * lda + c0 + c] = v;
   }
   cluster_sync_all();  // no CTA retires while a peer may still push into it
 }
@@ -534,7 +543,7 @@ constexpr size_t larfb_multi_smem(int rpc, int cs, int cw) {
 template <int CW>
 void larfb_multi_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv, const double2* T, double2* A,
                         long long lda, long long m, long long ncols, int nq, long long k, long long rpc, bool reverse,
-                        bool use_th) {
+                        bool use_th, const double2* ph, long long ph_ld, long long ph_col0) {
   static bool attr = false;
   if (!attr) {
     QT_CUDA(cudaFuncSetAttribute(larfb_multi_kernel<CW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -544,15 +553,18 @@ void larfb_multi_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv
   }
   QT_CUDA(cudaLaunchKernelEx(&cfg, larfb_multi_kernel<CW>, V, ldv, T, A, lda, static_cast<int>(m),
                              static_cast<int>(ncols), nq, static_cast<int>(k), static_cast<int>(rpc), reverse ? 1 : 0,
-                             use_th ? 1 : 0));
+                             use_th ? 1 : 0, ph, ph_ld, ph_col0));
 }
 
 // A (m x ncols <= 32, ld lda) <- H_{nq-1}^H ... H_0^H A with the reflectors of
 // panels 0..nq-1 stored in V (ld ldv; panel q in columns q*32.., from row q*32)
 // and T (32 x 32 per panel) of a k-column QR; false when m is too tall
 // (reverse = true, use_th = false: A <- H_0 ... H_{nq-1} A, the explicit-Q order)
+// (ph != nullptr: the written columns get the gauge phases of the diagonal of
+// ph (ld ph_ld) at global columns ph_col0 + c)
 bool larfb_multi(const double2* V, long long ldv, const double2* T, double2* A, long long lda, long long m,
-                 long long ncols, int nq, long long k, cudaStream_t st, bool reverse = false, bool use_th = true) {
+                 long long ncols, int nq, long long k, cudaStream_t st, bool reverse = false, bool use_th = true,
+                 const double2* ph = nullptr, long long ph_ld = 0, long long ph_col0 = 0) {
   const int max_cs = larfb_max_cs();
   if (max_cs == 0 || ncols <= 0 || ncols > NB) return false;
   if (nq <= 0) return true;
@@ -573,7 +585,7 @@ bool larfb_multi(const double2* V, long long ldv, const double2* T, double2* A, 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  larfb_multi_launch<8>(cfg, V, ldv, T, A, lda, m, ncols, nq, k, rpc, reverse, use_th);
+  larfb_multi_launch<8>(cfg, V, ldv, T, A, lda, m, ncols, nq, k, rpc, reverse, use_th, ph, ph_ld, ph_col0);
   QT_LAUNCHED();
   return true;
 }
