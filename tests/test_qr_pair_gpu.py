@@ -1,0 +1,107 @@
+"""The pipelined QR pair (qr_pair_pipelined: QR(X) with its reflectors applied
+to theta, QR(Y^H) one panel behind, explicit Q_n in blocks, explicit error by
+unitary invariance) against the oracle's alternating sweep
+(proj/src/gates.cpp:293-308, :343-450), at the sizes that take it: 256..2048
+rows, one sweep, no left_iso.  Ragged widths (eta not a multiple of the
+32-column panel), rectangular bonds, truncating and expanding policies, and the
+CBE scheme.  The same updates with the pair disabled (QT_NO_QR_PAIR is read
+once per process, so the comparison is against the oracle and across two
+bitwise-identical runs)."""
+import numpy as np
+import pytest
+
+from oracle import qrtebd_oracle as ref
+from paper_2212_09782_b200 import model
+from paper_2212_09782_b200 import qrtebd as q
+from test_gate_gpu import block_of, compare, random_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("d,chi,chi_l,chi_r,chi_max,dabs", [
+    (5, 64, 64, 64, 64, 0),        # rows 320, eta 64: two full panels
+    (5, 100, 100, 100, 100, 0),    # eta 100: ragged last panel (4 columns)
+    (4, 96, 80, 120, 70, 0),       # rectangular, truncating (eta = chi_max = 70)
+    (3, 128, 128, 128, 200, 60),   # expanding: eta = min(expanded, chi_max) = 188
+    (8, 64, 64, 64, 64, 0),        # rows = cols = 512
+    (5, 256, 256, 256, 256, 0),    # C2 shape: 1280 rows, 8 panels
+])
+def test_pair_qr_update_matches_oracle(ctx, d, chi, chi_l, chi_r, chi_max, dabs):
+    xi, bm, bn = random_inputs(d, chi, seed=7 * d + chi, chi_l=chi_l, chi_r=chi_r)
+    gate = model.make_gate(model.bond_hamiltonian(d, 2.0), 0.05)
+    pol = dict(chi_max=chi_max, sv_cutoff=1e-14, delta_chi_abs=dabs, delta_chi_rel=0.0)
+    o = ref.apply_gate_qr(xi, bm, bn, gate, ref.TruncationPolicy(**pol))
+    upd = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=False)
+    assert upd.left_iso is None
+    compare(upd, o, xi)
+    # Q_n and the bond matrix are gauge-fixed: compared directly (Appendix B (vi))
+    assert np.allclose(upd.b_n.numpy(), o.b_n, atol=1e-11)
+    assert np.allclose(upd.xi_n.numpy(), o.xi_n, atol=1e-12)
+    # bitwise run to run
+    upd2 = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=False)
+    assert np.array_equal(upd.b_m.numpy(), upd2.b_m.numpy())
+    assert np.array_equal(upd.b_n.numpy(), upd2.b_n.numpy())
+    assert upd.report.eps_trunc == upd2.report.eps_trunc
+
+
+@pytest.mark.parametrize("explicit", [True, False])
+def test_pair_explicit_error_small_and_large(ctx, explicit):
+    # near-exact update (eps ~ 1e-30 noise floor) and a strongly truncating one
+    d, chi = 5, 64
+    xi, bm, bn = random_inputs(d, chi, seed=99)
+    gate = model.make_gate(model.bond_hamiltonian(d, 2.0), 0.05)
+    for chi_max in (64, 20):
+        pol = dict(chi_max=chi_max, sv_cutoff=1e-14, delta_chi_abs=0, delta_chi_rel=0.0,
+                   compute_explicit_error=explicit)
+        o = ref.apply_gate_qr(xi, bm, bn, gate, ref.TruncationPolicy(**pol))
+        u = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=False)
+        assert abs(u.report.eps_trunc - o.report.eps_trunc) <= 1e-10 * o.report.eps_trunc + 1e-20
+        assert abs(u.report.discarded_weight - o.report.discarded_weight) <= 1e-9 * o.report.discarded_weight + 1e-15
+
+
+@pytest.mark.parametrize("d,chi,dabs", [(5, 64, 40), (3, 100, 30), (5, 256, 100)])
+def test_pair_cbe_update_matches_oracle(ctx, d, chi, dabs):
+    rng = np.random.default_rng(d * chi)
+    bm = ref.random_right_isometry(rng, d, chi, chi)
+    bn = ref.random_right_isometry(rng, d, chi, chi)
+    s = np.exp(-4.0 * np.arange(chi) / chi)
+    xi = np.diag(s / np.linalg.norm(s)).astype(complex)
+    gate = model.make_gate(model.bond_hamiltonian(d, 2.0), 0.05)
+    kw = dict(chi_max=chi, sv_cutoff=1e-14, delta_chi_abs=dabs, delta_chi_rel=0.1)
+    o = ref.apply_gate_qr_cbe(xi, bm, bn, gate, ref.TruncationPolicy(**kw))
+    u = q.apply_gate_qr_cbe(xi, bm, bn, gate, q.TruncationPolicy(**kw), ctx)
+    assert (u.report.chi_expanded, u.report.chi_after) == (o.report.chi_expanded, o.report.chi_after)
+    b_d = block_of(xi, u.b_m.numpy(), u.b_n.numpy())
+    b_o = block_of(xi, o.b_m, o.b_n)
+    assert np.linalg.norm(b_d - b_o) / np.linalg.norm(b_o) < 1e-10
+    s_d, s_o = np.diag(u.xi_n.numpy()).real, np.diag(o.xi_n).real
+    assert np.max(np.abs(s_d - s_o)) <= 1e-10 * s_o[0]
+    assert abs(u.report.eps_trunc - o.report.eps_trunc) <= 1e-10 * o.report.eps_trunc + 1e-20
+
+
+def test_pair_uniform_steps_match_oracle(ctx):
+    # a few device-resident C2-shaped steps (graph replay) against the oracle
+    d, chi = 5, 64
+    rng = np.random.default_rng(5)
+    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(2)]
+    bonds = []
+    for _ in range(2):
+        x = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+        bonds.append(x / np.linalg.norm(x))
+    sched = ref.trotter_schedule(ref.bond_hamiltonian(d, 2.0, "bulk"), 0.05, 2)
+    pol = ref.TruncationPolicy(chi_max=chi, sv_cutoff=1e-14, delta_chi_abs=0, delta_chi_rel=0.0)
+    dev = q.DeviceUniformMPS(q.UniformMPS.from_numpy(ctx, d, sites, bonds), ctx)
+    dsched = [(p, ctx.tensor(u)) for p, u in sched]
+    st = ref.UniformMPS(d, [s.copy() for s in sites], [b.copy() for b in bonds])
+    z = ref.clock_operators(d)[0]
+    for _ in range(4):
+        reps = dev.step(dsched, "qr", q.TruncationPolicy(chi_max=chi, sv_cutoff=1e-14, delta_chi_abs=0,
+                                                         delta_chi_rel=0.0))
+        st, oreps = ref.tebd_step_uniform(st, sched, "qr", pol)
+        for r, (_, o) in zip(reps, oreps):
+            assert abs(r.report.eps_trunc - o.eps_trunc) <= 1e-9 * o.eps_trunc + 2e-13 * o.eps_trunc ** 0.5 + 1e-20
+    snap = dev.snapshot()
+    for m in range(2):
+        zd = q.expectation_local(snap, z, m, ctx)
+        zo = ref.expectation_local(st, z, m)
+        assert abs(zd - zo) < 1e-10
