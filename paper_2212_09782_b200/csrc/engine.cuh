@@ -46,6 +46,7 @@ enum Slot : int {
   S_QR_V2,       // reflectors / T factors of the second QR of a pipelined pair
   S_QR_T2,
   S_GEMM_PART3,  // split-K scratch of GEMMs on side4 (consumers of the pair's Q blocks)
+  S_PY0,         // phiev Y0^H of the re-associated X = Xi (phiev Y0^H)
   S_TILE_SUMS3,
   S_COUNT
 };

@@ -252,7 +252,7 @@ void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, 
 }
 
 void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
-                 const double2* u, int out_scalar) {
+                 const double2* u, int out_scalar, bool phiev_only) {
   const long long d = D.d, cl = D.chi_l, cm = D.chi_m, cn = D.chi_n, cr = D.chi_r;
   const long long blk = cm * d * d * cr;
   double2* phi = e.cbuf(S_PHI, blk);
@@ -278,6 +278,7 @@ void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm,
     g.C = phiev; g.ldc = cr; g.strideC = d * d * cr;
     zgemm(g, gs, e.stream);
   }
+  if (phiev_only) return;
   // theta = Xi (cl x cm) . phiev (cm x d*d*cr)
   gemm(e, Op::N, Op::N, cl, d * d * cr, cm, xi, cm, phiev, d * d * cr, theta, d * d * cr);
   norm2(e, theta, cl, d * d * cr, d * d * cr, e.dscal + out_scalar);
@@ -289,7 +290,17 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   const long long rows = D.rows(), cols = D.cols();
   int* flag = reinterpret_cast<int*>(e.dscal + SC_TMP3);
   zero_flag_kernel<<<1, 1, 0, e.stream>>>(flag);
-  build_theta(e, D, xi, bm, bn, u, SC_THETA2);
+  const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
+  const bool qtheta = use_qtheta(pol, rows);
+  // QT_X_REASSOC=1 (pipelined pair with Y0 = B^n): X = Xi (phiev Y0^H) on the
+  // main stream while theta = Xi phiev is formed on the theta stream (first
+  // needed by the reflector of X's first panel); ||theta|| = ||Q_full^H theta||
+  // afterwards.  Measured no faster at C2 (194 vs 196 steps/s: the theta GEMM
+  // shares the SMs with X and the first panel), so off by default
+  static const bool reassoc = std::getenv("QT_X_REASSOC") != nullptr;
+  const bool pair = qtheta && !out.left_iso && use_qr_pair(rows, cols);
+  const bool x_reassoc = reassoc && pair && eta == cn && sweeps == 1;
+  build_theta(e, D, xi, bm, bn, u, SC_THETA2, x_reassoc);
   double2* phiev = e.cbuf(S_PHIEV, cm * d * d * cr);
   double2* theta = e.cbuf(S_THETA, cl * d * d * cr);
 
@@ -310,17 +321,32 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     permute(e, bn, 3, shp, perm, false, y);
     y0 = y;
   }
-  const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
   // Y = Q_m^H theta through the reflectors (one sweep, theta up to
   // QT_QTHETA_MAX_ROWS rows): each finished panel of QR(X) is applied to theta
   // on a side stream while the later panels factor, so when the panel chain
   // ends Q_full^H theta = [Y; Z] is ready -- no explicit Q_m (unless left_iso
   // is wanted), no theta^H Q_m GEMM, and the explicit error needs only
   // ||Y - L Q_n||^2 + ||Z||^2 instead of a theta-sized residual product
-  const bool qtheta = use_qtheta(pol, rows);
   bool hastings_done = false;
+  if (x_reassoc) {
+    // theta on the theta stream (side2), behind phiev
+    QT_CUDA(cudaEventRecord(e.event(0), e.stream));
+    QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(0), 0));
+    GemmDesc gt;
+    gt.M = cl; gt.N = d * d * cr; gt.K = cm;
+    gt.A = xi; gt.lda = cm;
+    gt.B = phiev; gt.ldb = d * d * cr;
+    gt.C = theta; gt.ldc = d * d * cr;
+    zgemm(gt, e.gemm_scratch2(), e.side2);
+    // P = phiev Y0^H ((cm d) x eta), X = Xi P viewed as (cm) x (d eta) -> (cl d) x eta
+    double2* P = e.cbuf(S_PY0, cm * d * eta);
+    gemm(e, Op::N, Op::H, cm * d, eta, cols, phiev, cols, y0, cols, P, eta);
+    gemm(e, Op::N, Op::N, cl, d * eta, cm, xi, cm, P, d * eta, X, d * eta);
+  }
   for (int it = 0; it < sweeps; ++it) {
-    if (it == 0)
+    if (it == 0 && x_reassoc)
+      ;  // X formed above
+    else if (it == 0)
       gemm(e, Op::N, Op::H, rows, eta, cols, theta, cols, y0, cols, X, eta);  // X = theta Y0^H
     else
       gemm(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);   // Y0 = Q_n = Qp^H
@@ -349,6 +375,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
           hastings_block);
       hastings_done = static_cast<bool>(hastings_block);
       check_finite(e, theta, eta * cols, flag);  // Y (the first eta rows of Q_full^H theta)
+      if (x_reassoc) norm2(e, theta, rows, cols, cols, e.dscal + SC_THETA2);  // ||Q_full^H theta|| = ||theta||
       continue;
     }
     if (qtheta) {
