@@ -14,8 +14,10 @@
 //   Xi~ = L/|L|, B~n = Q_n -> (d,eta,chi_r), B~m = phiev Q_n^H (permuted store),
 //   left_iso = Q_m -> (d,chi_l,eta), eps = ||theta - Q_m L Q_n||^2/||theta||^2
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "gate.cuh"
 
@@ -288,6 +290,21 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
                    const double2* u, const qt_policy& pol, long long eta, const GateBuffers& out) {
   const long long d = D.d, cl = D.chi_l, cm = D.chi_m, cn = D.chi_n, cr = D.chi_r;
   const long long rows = D.rows(), cols = D.cols();
+  // QT_UPDATE_DEBUG=1 (eager calls only): phase durations of the update on stderr
+  static const bool udbg = std::getenv("QT_UPDATE_DEBUG") != nullptr;
+  static std::vector<cudaEvent_t> uev;
+  std::vector<const char*> unm;
+  auto ustamp = [&](const char* nm) {
+    if (!udbg) return;
+    if (uev.size() <= unm.size()) {
+      cudaEvent_t ev;
+      QT_CUDA(cudaEventCreate(&ev));
+      uev.push_back(ev);
+    }
+    QT_CUDA(cudaEventRecord(uev[unm.size()], e.stream));
+    unm.push_back(nm);
+  };
+  ustamp("start");
   int* flag = reinterpret_cast<int*>(e.dscal + SC_TMP3);
   zero_flag_kernel<<<1, 1, 0, e.stream>>>(flag);
   const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
@@ -301,6 +318,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   const bool pair = qtheta && !out.left_iso && use_qr_pair(rows, cols);
   const bool x_reassoc = reassoc && pair && eta == cn && sweeps == 1;
   build_theta(e, D, xi, bm, bn, u, SC_THETA2, x_reassoc);
+  ustamp("theta");
   double2* phiev = e.cbuf(S_PHIEV, cm * d * d * cr);
   double2* theta = e.cbuf(S_THETA, cl * d * d * cr);
 
@@ -351,6 +369,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     else
       gemm(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);   // Y0 = Q_n = Qp^H
     check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
+    ustamp("X");
     if (qtheta && !out.left_iso && use_qr_pair(rows, cols)) {
       // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
       // QT_QB_HASTINGS=1: the Hastings columns of B~m follow the Q blocks of
@@ -376,6 +395,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
       hastings_done = static_cast<bool>(hastings_block);
       check_finite(e, theta, eta * cols, flag);  // Y (the first eta rows of Q_full^H theta)
       if (x_reassoc) norm2(e, theta, rows, cols, cols, e.dscal + SC_THETA2);  // ||Q_full^H theta|| = ||theta||
+      ustamp("pair");
       continue;
     }
     if (qtheta) {
@@ -409,6 +429,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     const int perm[3] = {0, 2, 1};
     permute(e, Qp, 3, shp, perm, true, out.b_n);
   }
+  ustamp("xi_bn");
   if (out.b_m && !hastings_done) {
     // B~m[i,beta,k] = sum_{j,delta} phiev[beta,i,j,delta] conj(B~n[j,k,delta])
     //             = (phiev (cm*d x d*cr) . Qp)[(beta i), k]   (gates.cpp:186-190)
@@ -443,6 +464,17 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     g.C = theta; g.ldc = cols;
     g.mode = GemmMode::resid;
     zgemm(g, e.gemm_scratch(), e.stream, e.dscal + SC_RESID);
+  }
+  ustamp("end");
+  if (udbg) {
+    QT_CUDA(cudaStreamSynchronize(e.stream));
+    std::fprintf(stderr, "update rows=%lld cols=%lld eta=%lld phases (us):", rows, cols, eta);
+    for (size_t k = 1; k < unm.size(); ++k) {
+      float ms = 0.f;
+      QT_CUDA(cudaEventElapsedTime(&ms, uev[k - 1], uev[k]));
+      std::fprintf(stderr, " %s=%.0f", unm[k], ms * 1000.f);
+    }
+    std::fprintf(stderr, "\n");
   }
 }
 

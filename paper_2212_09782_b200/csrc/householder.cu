@@ -20,6 +20,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -387,7 +388,7 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp, cudaStream_t s
 // split-K scratch belong to that stream)
 void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, double2* C, long long ldc,
                            long long mp, long long nc, int nbp, double2* W, double2* W2, const GemmScratch& gs,
-                           cudaStream_t st) {
+                           cudaStream_t st, const std::function<void()>& after_top = nullptr) {
   GemmDesc g;
   g.M = nbp; g.N = nc; g.K = mp;
   g.opA = Op::H; g.A = Vp; g.lda = ldv;
@@ -400,13 +401,24 @@ void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, 
   g2.opB = Op::N; g2.B = W; g2.ldb = nc;
   g2.C = W2; g2.ldc = nc;
   zgemm(g2, gs, st);
+  // C -= V W2; with after_top: the first nbp rows first (the block the caller
+  // publishes next), then the callback, then the remaining rows
+  const long long top = after_top ? std::min<long long>(nbp, mp) : mp;
   GemmDesc g3;
-  g3.M = mp; g3.N = nc; g3.K = nbp;
+  g3.M = top; g3.N = nc; g3.K = nbp;
   g3.opA = Op::N; g3.A = Vp; g3.lda = ldv;
   g3.opB = Op::N; g3.B = W2; g3.ldb = nc;
   g3.C = C; g3.ldc = ldc;
   g3.alpha = -1.0; g3.beta = 1.0;
   zgemm(g3, gs, st);
+  if (!after_top) return;
+  after_top();
+  if (mp > top) {
+    g3.M = mp - top;
+    g3.A = Vp + top * ldv;
+    g3.C = C + top * ldc;
+    zgemm(g3, gs, st);
+  }
 }
 
 }  // namespace
@@ -665,10 +677,13 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     // ---- theta side: C <- H_p^H C, then rows [j, j + nbp) of C are final
     QT_CUDA(cudaEventRecord(e.event(P0 + p), sx));
     QT_CUDA(cudaStreamWaitEvent(sa, e.event(P0 + p), 0));
-    apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa);
-    extract(j, nbp, sa);
-    stamp("extract" + std::to_string(p), sa);
-    QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
+    // rows [j, j + nbp) of H_p^H C are final first: publish them as block p of
+    // Y^H before the rest of C is updated
+    apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa, [&] {
+      extract(j, nbp, sa);
+      stamp("extract" + std::to_string(p), sa);
+      QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
+    });
     // ---- X trailing update (look-ahead: next panel's columns on sx, the rest on sxw)
     const long long ntr = k - j - nbp;
     if (ntr > 0) {

@@ -298,6 +298,8 @@ bool larfb_cluster(Engine& e, const double2* V, long long ldv, const double2* T,
     cw = 8;
   else if (ceil_div(ncols, 16) <= 8)
     cw = 16;
+  static const int cw_narrow = std::getenv("QT_NARROW_CW") ? std::atoi(std::getenv("QT_NARROW_CW")) : 0;
+  if (ncols <= NB && (cw_narrow == 8 || cw_narrow == 16 || cw_narrow == 32)) cw = cw_narrow;
   static const bool dbg_on = std::getenv("QT_LARFB_DEBUG") != nullptr;
   static long long* dbg = nullptr;
   if (dbg_on && !dbg) QT_CUDA(cudaMalloc(&dbg, 16 * sizeof(long long)));
