@@ -66,6 +66,12 @@ struct PanelArgs {
   double2* diag;   // [2][32] broadcast of the current diagonal row
   unsigned* bar;   // grid barrier words
   long long* dbg;  // optional per-column clock64 stamps (CTA 0, thread 0)
+  // fused look-ahead (cluster panel, pre != 0): before factoring, apply the
+  // previous panel's block reflector H_{p-1}^H to this panel's columns -- the
+  // panel rows and the 32 rows above them (R12, A12 = A - 32 lda)
+  const double2* vprev = nullptr;  // V_{p-1} at its own top row (32 rows above A), ld ldv
+  const double2* tprev = nullptr;  // T_{p-1} (32 x 32)
+  int pre = 0;
 };
 
 __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_kernel(PanelArgs a) {
@@ -270,17 +276,26 @@ int grid_for(long long total) {
 template <int RPW>
 void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs, cudaStream_t st) {
   auto kern = panel_cluster_kernel<RPW>;
+  // the fused look-ahead stages (32 + rows) x 32 V and A tiles: RPW <= 5 (smem)
+  constexpr size_t pre_smem = [] {
+    size_t mx = 0;  // the reduce-scatter inbox depends on the cluster size: max over 1..16
+    for (int c = 1; c <= 16; ++c) mx = panel_pre_smem<RPW>(c) > mx ? panel_pre_smem<RPW>(c) : mx;
+    return RPW <= 5 ? mx : size_t(0);
+  }();
+  constexpr size_t smem_attr = pre_smem > panel_cluster_smem(RPW) ? pre_smem : panel_cluster_smem(RPW);
   static bool attr = false;
   if (!attr) {
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(panel_cluster_smem(RPW))));
+    QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_attr)));
     attr = true;
   }
+  if (a.pre && RPW > 5) throw Error(Err::internal, "fused panel look-ahead needs <= 5 rows per warp");
+  const size_t smem = a.pre ? std::max(panel_cluster_smem(RPW), panel_pre_smem<RPW>(static_cast<int>(cs)))
+                            : panel_cluster_smem(RPW);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(cs));
   cfg.blockDim = dim3(CL_THREADS);
-  cfg.dynamicSmemBytes = panel_cluster_smem(RPW);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -602,6 +617,15 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 
 bool qr_pair_fits(long long m, long long nc) { return larfb_cluster_fits(m) && larfb_cluster_fits(nc); }
 
+namespace {
+// the cluster panel for mp rows would run with <= 5 rows per warp (fused look-ahead)
+bool panel_pre_fits(long long mp) {
+  static const int cs_cap = std::getenv("QT_PANEL_CS") ? std::atoi(std::getenv("QT_PANEL_CS")) : 16;
+  const long long cs_max = std::max(1, std::min(16, cs_cap));
+  return ceil_div(mp, cs_max * CL_WARPS) <= 5;
+}
+}  // namespace
+
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
                        double2* qy, double2* ry,
                        const std::function<void(long long, long long, cudaStream_t)>& extract,
@@ -660,6 +684,13 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
   stamp("start", sx);
   bool wide_pending = false;
   long long last_wide = -1;
+  // QT_FUSED_PANEL=1: the look-ahead block update fused into the next panel
+  // (PanelArgs::pre) instead of a separate narrow block-reflector launch.
+  // Measured no faster at C2 (192 vs 195 steps/s: the in-panel update on the
+  // panel's 16 CTAs costs what the 40-CTA launch did), so off by default
+  static const bool fused_env = std::getenv("QT_FUSED_PANEL") != nullptr;
+  const bool fused = fused_env && panel_pre_fits(m) && panel_pre_fits(nc);
+  std::vector<bool> wide_of(static_cast<size_t>(npan), false);
   for (long long p = 0; p < npan; ++p) {
     const long long j = p * NB;
     const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
@@ -672,6 +703,13 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     pa.V = Vx + j * kp + p * NB;
     pa.ldv = kp;
     pa.T = Tx + p * NB * NB;
+    if (fused && p > 0) {
+      // block p: H_0..H_{p-2} came with the wide updates, H_{p-1} is fused into the panel
+      if (p >= 2 && wide_of[p - 2]) QT_CUDA(cudaStreamWaitEvent(sx, e.event(2 * (p - 2) + 1), 0));
+      pa.pre = 1;
+      pa.vprev = Vx + (j - NB) * kp + (p - 1) * NB;
+      pa.tprev = Tx + (p - 1) * NB * NB;
+    }
     launch_panel(e, pa, m - j, sx);
     stamp("Xpanel" + std::to_string(p), sx);
     // ---- theta side: C <- H_p^H C, then rows [j, j + nbp) of C are final
@@ -686,7 +724,19 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     });
     // ---- X trailing update (look-ahead: next panel's columns on sx, the rest on sxw)
     const long long ntr = k - j - nbp;
-    if (ntr > 0) {
+    if (fused && ntr > 0) {
+      // next panel's columns: fused into that panel; the rest on sxw
+      const long long nn = std::min<long long>(NB, ntr);
+      if (ntr > nn) {
+        QT_CUDA(cudaEventRecord(e.event(2 * p), sx));
+        QT_CUDA(cudaStreamWaitEvent(sxw, e.event(2 * p), 0));
+        larfb_cluster(e, pa.V, kp, pa.T, x + j * k + j + nbp + nn, k, m - j, ntr - nn, nbp, true, sxw);
+        stamp("Xwide" + std::to_string(p), sxw);
+        QT_CUDA(cudaEventRecord(e.event(2 * p + 1), sxw));
+        wide_of[p] = true;
+        last_wide = p;
+      }
+    } else if (ntr > 0) {
       const long long nn = std::min<long long>(NB, ntr);
       if (p > 0 && wide_pending) QT_CUDA(cudaStreamWaitEvent(sx, e.event(2 * (p - 1) + 1), 0));
       if (ntr > nn) {
@@ -718,7 +768,7 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
       QT_CUDA(cudaStreamWaitEvent(sy, e.event(E0 + p), 0));
     }
     stamp("Ystart" + std::to_string(p), sy);
-    if (p >= 1) {
+    if (p >= 1 && !fused) {
       const long long jq = (p - 1) * NB;
       larfb_cluster(e, Vy + jq * kp + (p - 1) * NB, kp, Ty + (p - 1) * NB * NB, yh + jq * k + j, k, nc - jq, nbp, NB,
                     true, sy);
@@ -731,6 +781,11 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     py.V = Vy + j * kp + p * NB;
     py.ldv = kp;
     py.T = Ty + p * NB * NB;
+    if (fused && p >= 1) {  // H'_{p-1} fused into Y panel p
+      py.pre = 1;
+      py.vprev = Vy + (j - NB) * kp + (p - 1) * NB;
+      py.tprev = Ty + (p - 1) * NB * NB;
+    }
     stamp("Yupdate" + std::to_string(p), sy);
     launch_panel(e, py, nc - j, sy);
     stamp("Ypanel" + std::to_string(p), sy);
