@@ -523,8 +523,8 @@ __global__ void jacobi_setup_kernel(const double2* __restrict__ h, int n, int N,
 
 // sort the N diagonal entries descending (ties: lower index first), write the
 // first n eigenvalues and the matching eigenvector columns (n x n, ld n)
-__global__ void jacobi_sort_kernel(const double2* __restrict__ G, const double2* __restrict__ V, int n, int N,
-                                   const double* fro, double* w, double2* vout) {
+__global__ void jacobi_sort_kernel(const double2* __restrict__ G, int n, int N, const double* fro, double* w,
+                                   int* idx_out) {
   extern __shared__ unsigned char jsm[];
   int P = 1;
   while (P < N) P <<= 1;
@@ -557,8 +557,18 @@ __global__ void jacobi_sort_kernel(const double2* __restrict__ G, const double2*
     }
   }
   const double inv_sc = 1.0 / jscale(fro);  // exact (power of two)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = k2[i] * inv_sc;
-  for (long long e = threadIdx.x; e < static_cast<long long>(n) * n; e += blockDim.x) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    w[i] = k2[i] * inv_sc;
+    idx_out[i] = idx[i];
+  }
+}
+
+// eigenvectors in the sorted order: vout[r, c] = V[r, idx[c]] (grid-wide; one
+// CTA per row block, the permuted reads stay inside a 16 N-byte row)
+__global__ void jacobi_gather_kernel(const double2* __restrict__ V, int n, int N, const int* __restrict__ idx,
+                                     double2* __restrict__ vout) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(n) * n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(e / n), c = static_cast<int>(e % n);
     vout[e] = V[static_cast<long long>(r) * N + idx[c]];
   }
@@ -592,7 +602,8 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   const int ngt = npairs * (npairs + 1) / 2;
   const int grid = std::min(e.num_sms, std::max(2 * npairs, std::min(ngt + (N / JX) * npairs, e.num_sms)));
   if (grid <= npairs) throw Error(Err::capacity, "eigh: matrix too large for the cooperative Jacobi kernel");
-  double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8 + ngt / 2 + 1);
+  // [cta_max 2 grid][sweeps 8][tflag ngt/2+1][sorted index n/2+1] (doubles)
+  double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8 + ngt / 2 + 1 + static_cast<size_t>(n) / 2 + 2);
   int* sweeps = reinterpret_cast<int*>(cta_max + 2 * grid);
   unsigned* tflag = reinterpret_cast<unsigned*>(cta_max + 2 * grid + 8);
   jacobi_setup_kernel<<<static_cast<int>(std::min<long long>(ceil_div(static_cast<long long>(N) * N, 256), 2048)), 256,
@@ -671,7 +682,12 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
                                  static_cast<int>(smem)));
     attr = smem;
   }
-  jacobi_sort_kernel<<<1, 1024, smem, e.stream>>>(G, V, static_cast<int>(n), N, fro, w, v);
+  int* idx = reinterpret_cast<int*>(cta_max + 2 * grid + 8 + ngt / 2 + 1);
+  jacobi_sort_kernel<<<1, 1024, smem, e.stream>>>(G, static_cast<int>(n), N, fro, w, idx);
+  QT_LAUNCHED();
+  const long long nn = static_cast<long long>(n) * n;
+  jacobi_gather_kernel<<<static_cast<int>(std::min<long long>(ceil_div(nn, 256), 4 * e.num_sms)), 256, 0, e.stream>>>(
+      V, static_cast<int>(n), N, idx, v);
   QT_LAUNCHED();
 }
 
