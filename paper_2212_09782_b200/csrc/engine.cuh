@@ -47,6 +47,10 @@ enum Slot : int {
   S_QR_T2,
   S_GEMM_PART3,  // split-K scratch of GEMMs on side4 (consumers of the pair's Q blocks)
   S_PY0,         // phiev Y0^H of the re-associated X = Xi (phiev Y0^H)
+  S_QR_WS,       // W / W2 of the QR look-ahead's wide updates on e.side (GEMM path)
+  S_QR_WS2,
+  S_GEMM_PARTS,  // split-K scratch of GEMMs on e.side
+  S_TILE_SUMSS,
   S_TILE_SUMS3,
   S_COUNT
 };

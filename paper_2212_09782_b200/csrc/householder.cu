@@ -463,10 +463,30 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   if (dbg_on && !dbg_buf) QT_CUDA(cudaMalloc(&dbg_buf, 8 * NB * sizeof(long long)));
   base.dbg = dbg_on ? dbg_buf : nullptr;
 
-  // look-ahead of the trailing update when every block reflector fits one
-  // cluster (m <= 16 x 128); QT_QR_NO_LOOKAHEAD disables it
+  // look-ahead of the trailing update: the next panel's columns on the main
+  // stream, the rest on e.side behind the next panel -- block reflectors in one
+  // cluster launch when m <= 16 x 128, else as three DMMA GEMMs per update
+  // (each stream with its own W buffers and split-K scratch);
+  // QT_QR_NO_LOOKAHEAD disables it
   static const bool la_env = std::getenv("QT_QR_NO_LOOKAHEAD") == nullptr;
-  const bool lookahead = la_env && npan >= 2 && e.side != nullptr && larfb_cluster_fits(m);
+  // QT_QR_GEMM_LA_MAX=m: the GEMM look-ahead for taller panels up to m rows
+  // (QR 5120 x 1024: 9.63 -> 9.09 ms, but the north-star step moves < 0.5%
+  // and the 8-stream C5 chain loses 4%: off by default)
+  static const long long la_gemm_max = std::getenv("QT_QR_GEMM_LA_MAX")
+                                           ? std::atoll(std::getenv("QT_QR_GEMM_LA_MAX"))
+                                           : 0;
+  const bool la_cluster = larfb_cluster_fits(m);
+  const bool lookahead = la_env && npan >= 2 && e.side != nullptr && (la_cluster || m <= la_gemm_max);
+  double2 *SW = nullptr, *SW2 = nullptr;
+  GemmScratch gss;
+  if (lookahead && !la_cluster) {
+    SW = e.cbuf(S_QR_WS, static_cast<size_t>(NB) * n);
+    SW2 = e.cbuf(S_QR_WS2, static_cast<size_t>(NB) * n);
+    gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
+    gss.partial_elems = size_t(1) << 22;
+    gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
+    gss.tile_sums_elems = size_t(1) << 16;
+  }
   bool wide_pending = false;
   long long last_wide = -1;
   // QrOpts::capply: panel p's reflector reaches C on side2 once the panel is
@@ -527,10 +547,17 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
         QT_CUDA(cudaEventRecord(e.event(2 * p), e.stream));  // panel p done: V_p, T_p ready
         QT_CUDA(cudaStreamWaitEvent(e.side, e.event(2 * p), 0));
       }
-      larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, nn, nbp, true, e.stream);
+      if (la_cluster)
+        larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, nn, nbp, true, e.stream);
+      else
+        apply_block_reflector(pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, nn, nbp, W, W2, gs, e.stream);
       wide_pending = ntr > nn;
       if (wide_pending) {
-        larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp + nn, lda, mp, ntr - nn, nbp, true, e.side);
+        if (la_cluster)
+          larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp + nn, lda, mp, ntr - nn, nbp, true, e.side);
+        else
+          apply_block_reflector(pa.V, kp, pa.T, a + j * lda + j + nbp + nn, lda, mp, ntr - nn, nbp, SW, SW2, gss,
+                                e.side);
         QT_CUDA(cudaEventRecord(e.event(2 * p + 1), e.side));
         last_wide = p;
       }

@@ -71,7 +71,8 @@ int main(int argc, char** argv) {
     }
     return best * 1000.f;
   };
-  printf("pipelined pair (QR(X) + apply + QR(Y^H) + Q_y): %.1f us\n", run_pair());
+  if (qr_pair_fits(m, nc) && n <= m && n <= nc)
+    printf("pipelined pair (QR(X) + apply + QR(Y^H) + Q_y): %.1f us\n", run_pair());
   printf("m=%lld n=%lld nc=%lld: QR with Q+R %.1f us | QR + apply to C (no Q) %.1f us | QR + apply + Q %.1f us\n", m,
          n, nc, run(0), run(1), run(2));
   return 0;

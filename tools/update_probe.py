@@ -2,7 +2,8 @@ import sys, os, numpy as np
 sys.path.insert(0, os.getcwd())
 from paper_2212_09782_b200 import qrtebd as q, model
 ctx = q.Context(0)
-d, chi = 5, 256
+import os
+d, chi = int(os.environ.get("D", 5)), int(os.environ.get("CHI", 256))
 rng = np.random.default_rng(1)
 bm = model.random_right_isometry(rng, d, chi, chi); bn = model.random_right_isometry(rng, d, chi, chi)
 xi = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi)); xi /= np.linalg.norm(xi)
