@@ -105,3 +105,30 @@ def test_pair_uniform_steps_match_oracle(ctx):
         zd = q.expectation_local(snap, z, m, ctx)
         zo = ref.expectation_local(st, z, m)
         assert abs(zd - zo) < 1e-10
+
+
+def test_pair_concurrent_cell_L4_matches_oracle(ctx):
+    # L = 4: the two same-parity updates of a layer run on concurrent engines,
+    # each with its own six-stream pipelined pair, inside one captured graph
+    d, chi, L = 5, 64, 4
+    rng = np.random.default_rng(44)
+    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(L)]
+    bonds = []
+    for _ in range(L):
+        x = rng.standard_normal((chi, chi)) + 1j * rng.standard_normal((chi, chi))
+        bonds.append(x / np.linalg.norm(x))
+    sched = ref.trotter_schedule(ref.bond_hamiltonian(d, 2.0, "bulk"), 0.05, 2)
+    kw = dict(chi_max=chi, sv_cutoff=1e-14, delta_chi_abs=0, delta_chi_rel=0.0)
+    dev = q.DeviceUniformMPS(q.UniformMPS.from_numpy(ctx, d, sites, bonds), ctx)
+    dsched = [(p, ctx.tensor(u)) for p, u in sched]
+    st = ref.UniformMPS(d, [s.copy() for s in sites], [b.copy() for b in bonds])
+    for _ in range(3):
+        dev.step(dsched, "qr", q.TruncationPolicy(**kw))
+        st, _ = ref.tebd_step_uniform(st, sched, "qr", ref.TruncationPolicy(**kw))
+    snap = dev.snapshot()
+    z = ref.clock_operators(d)[0]
+    for m in range(L):
+        assert abs(q.expectation_local(snap, z, m, ctx) - ref.expectation_local(st, z, m)) < 1e-10
+        sd = q.schmidt_values(snap, m, ctx)
+        so = ref.schmidt_values(st, m)
+        assert np.max(np.abs(sd[: len(so)] - so)[so >= 1e-6 * so[0]]) <= 1e-10 * so[0]
