@@ -25,6 +25,8 @@ pytestmark = pytest.mark.gpu
     (3, 128, 128, 128, 200, 60),   # expanding: eta = min(expanded, chi_max) = 188
     (8, 64, 64, 64, 64, 0),        # rows = cols = 512
     (5, 256, 256, 256, 256, 0),    # C2 shape: 1280 rows, 8 panels
+    (5, 20, 64, 64, 20, 0),        # eta = 20 < one panel on 320 x 320
+    (5, 40, 64, 56, 40, 0),        # eta = 40: one full panel + 8 columns
 ])
 def test_pair_qr_update_matches_oracle(ctx, d, chi, chi_l, chi_r, chi_max, dabs):
     xi, bm, bn = random_inputs(d, chi, seed=7 * d + chi, chi_l=chi_l, chi_r=chi_r)
