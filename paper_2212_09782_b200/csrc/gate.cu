@@ -13,6 +13,12 @@
 //   X = theta Y0^H ; QR ; Y^H = theta^H Q ; QR      DMMA GEMMs + K3 (gates.cpp:293-308)
 //   Xi~ = L/|L|, B~n = Q_n -> (d,eta,chi_r), B~m = phiev Q_n^H (permuted store),
 //   left_iso = Q_m -> (d,chi_l,eta), eps = ||theta - Q_m L Q_n||^2/||theta||^2
+//
+// For one sweep on 256..2048-row matrices the two QRs run as a pipelined pair
+// (qr_pair_pipelined, householder.cu): each QR(X) panel's reflector is applied
+// to theta behind the panel chain, so Q_full^H theta = [Y; Z] replaces the
+// explicit Q_m and the theta^H Q_m product, QR(Y^H) runs one panel behind on
+// its own stream, and eps = (||Y - L Q_n||^2 + ||Z||^2) / ||theta||^2.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
