@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--max-chi", type=int, default=1024)
     a = ap.parse_args()
     ctx = q.Context(0)
+    peak = ctx.fp64_peak(0)
     cells = [(d, 64) for d in (5, 8, 11, 14, 17, 20)] + [(5, c) for c in (128, 256, 512, 1024) if c <= a.max_chi]
     for d, chi in cells:
         xi, bm, bn, u = inputs(d, chi)
@@ -57,7 +58,12 @@ def main():
         sync = torch.cuda.synchronize
         t_svd = timed(lambda: apply_gate_svd_gpu(*tt, pol), max(1, a.reps), sync)
         t_eig = timed(lambda: apply_gate_eig_gpu(*tt, pol), max(1, a.reps), sync)
-        print(json.dumps({"d": d, "chi": chi, "qr_ms": t_qr * 1e3, "svd_ms": t_svd * 1e3, "eig_ms": t_eig * 1e3,
+        # algorithmic flops of the QR update (explicit error off, eta = kk = chi)
+        f = 8.0 * (2 * d * d * chi ** 3 + d ** 4 * chi ** 2 + 3 * d * d * chi * chi * chi) + \
+            2.0 * (16.0 * (d * chi) * chi * chi - 16.0 / 3.0 * chi ** 3)
+        print(json.dumps({"d": d, "chi": chi, "qr_ms": t_qr * 1e3, "qr_updates_per_s": 1.0 / t_qr,
+                          "qr_tflops": f / t_qr / 1e12, "qr_frac_of_dmma_peak": f / t_qr / 1e12 / peak,
+                          "svd_ms": t_svd * 1e3, "eig_ms": t_eig * 1e3,
                           "svd_over_qr": t_svd / t_qr, "eig_over_qr": t_eig / t_qr}), flush=True)
 
 
