@@ -207,15 +207,24 @@ constexpr int kNormBlocks = 296;
 
 __global__ void norm2_partial_kernel(const double2* __restrict__ x, long long rows, long long cols, long long ld,
                                      double* part) {
+  // block b sums rows b, b + gridDim.x, ... (no per-element index division;
+  // two accumulation chains); fixed assignment and order -> deterministic
   __shared__ double sh[256];
-  double s = 0.0;
-  const long long total = rows * cols;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = e / cols, c = e % cols;
-    const double2 v = x[r * ld + c];
-    s = fma(v.x, v.x, fma(v.y, v.y, s));
+  double s = 0.0, s1 = 0.0;
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const double2* row = x + r * ld;
+    long long c = threadIdx.x;
+    for (; c + blockDim.x < cols; c += 2 * blockDim.x) {
+      const double2 v = row[c], w = row[c + blockDim.x];
+      s = fma(v.x, v.x, fma(v.y, v.y, s));
+      s1 = fma(w.x, w.x, fma(w.y, w.y, s1));
+    }
+    if (c < cols) {
+      const double2 v = row[c];
+      s = fma(v.x, v.x, fma(v.y, v.y, s));
+    }
   }
+  s += s1;
   sh[threadIdx.x] = s;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {

@@ -289,7 +289,7 @@ void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm,
   if (phiev_only) return;
   // theta = Xi (cl x cm) . phiev (cm x d*d*cr)
   gemm(e, Op::N, Op::N, cl, d * d * cr, cm, xi, cm, phiev, d * d * cr, theta, d * d * cr);
-  norm2(e, theta, cl, d * d * cr, d * d * cr, e.dscal + out_scalar);
+  norm2(e, theta, cl * d, d * cr, d * cr, e.dscal + out_scalar);  // (alpha i) x (j delta) view: more rows
 }
 
 void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
