@@ -382,17 +382,33 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
       // Y^H (column block b of B~m = phiev Qp[:, b] as soon as that block of Qp
       // exists); measured slower at C2 (172 vs 181 steps/s: the per-block
       // GEMMs contend with both panel chains), so off by default
+      //
+      // QT_HASTINGS_SPLIT=1: two Hastings GEMMs -- the columns of every Q
+      // block but the last, issued on the Q stream once the next-to-last block
+      // exists (overlapping the last Y panel and the last Q block), and the
+      // last block's columns after it; measured 192 vs 194.5 steps/s at C2
+      // (the GEMM delays the last panel), so off by default
       const GemmScratch gs3 = e.gemm_scratch3();
       std::function<void(long long, long long, cudaStream_t)> hastings_block;
       static const bool qb_hastings = std::getenv("QT_QB_HASTINGS") != nullptr;
+      static const bool split_hastings =
+          std::getenv("QT_HASTINGS_SPLIT") && std::atoi(std::getenv("QT_HASTINGS_SPLIT")) != 0;
+      const long long npan_y = ceil_div(eta, 32);
+      auto hastings_cols = [&, gs3](long long c0, long long nb, cudaStream_t st) {
+        GemmDesc g;
+        g.M = cm * d; g.N = nb; g.K = cols;
+        g.A = phiev; g.lda = cols;
+        g.B = Qp + c0; g.ldb = eta;
+        g.C = out.b_m + c0; g.ldc = cm * eta; g.rsplit = d; g.ldc_hi = eta;
+        zgemm(g, gs3, st);
+      };
       if (out.b_m && qb_hastings)
-        hastings_block = [&](long long c0, long long nb, cudaStream_t st) {
-          GemmDesc g;
-          g.M = cm * d; g.N = nb; g.K = cols;
-          g.A = phiev; g.lda = cols;
-          g.B = Qp + c0; g.ldb = eta;
-          g.C = out.b_m + c0; g.ldc = cm * eta; g.rsplit = d; g.ldc_hi = eta;
-          zgemm(g, gs3, st);
+        hastings_block = hastings_cols;
+      else if (out.b_m && split_hastings && npan_y >= 3)
+        hastings_block = [&, hastings_cols](long long c0, long long nb, cudaStream_t st) {
+          const long long b = c0 / 32;
+          if (b == npan_y - 2) hastings_cols(0, c0 + nb, st);  // blocks 0 .. npan-2
+          else if (b == npan_y - 1) hastings_cols(c0, nb, st);  // the last block
         };
       qr_pair_pipelined(
           e, X, rows, eta, theta, cols, YH, Qp, Rp,
