@@ -472,32 +472,43 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
     }
   }
   if (rank != 0) return;
-  // z vectors of the T recurrence (zlarft), l < c (all scales are final):
-  //   z_l = -tau_c (conj(v_c,l) + scale_c h_l),  v_c,l = scale_l x^(l)_c,  h_l = conj(scale_l) conj(p_l)
-  for (int c = w; c < nbp; c += CL_WARPS) {
-    const double2 dk = Z[c * NB + k], sk = Ts[c * NB + k], tc = taus[c], scl = scales[c];
-    Z[c * NB + k] = (k < c) ? cmul(make_double2(-tc.x, -tc.y), cadd(cconj(cmul(my_scale, dk)),
-                                                                   cmul(scl, cmul(cconj(my_scale), cconj(sk)))))
-                            : make_double2(0.0, 0.0);
+  // T factor (zlarft, forward columnwise) on CTA 0 from the Gram entries of
+  // the reflectors, M[l][c] = v_l^H v_c (l < c; all scales are final):
+  //   v_c,l = scale_l x^(l)_c,  h_l = conj(scale_l) conj(p_l),  M = conj(v_c,l) + scale_c h_l
+  // stored transposed (Z[c][l] = M[l][c]), zero on and below the diagonal and
+  // past the panel width
+  for (int c = w; c < NB; c += CL_WARPS) {
+    double2 m = make_double2(0.0, 0.0);
+    if (c < nbp && k < c) {
+      const double2 dk = Z[c * NB + k], sk = Ts[c * NB + k], scl = scales[c];
+      m = cadd(cconj(cmul(my_scale, dk)), cmul(scl, cmul(cconj(my_scale), cconj(sk))));
+    }
+    Z[c * NB + k] = m;
+  }
+  for (int e = threadIdx.x; e < NB * NB; e += CL_THREADS) {
+    const int i = e / NB, j = e % NB;
+    Ts[e] = (i == j && i < nbp) ? taus[i] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  // zlarft (forward, columnwise) on CTA 0: T[c,c] = tau_c, T[0:c,c] = T[0:c,0:c] z_c;
-  // each column's triangular product is spread over the 16 warps
-  for (int e = threadIdx.x; e < NB * NB; e += CL_THREADS) Ts[e] = make_double2(0.0, 0.0);
-  __syncthreads();
-  if (threadIdx.x < nbp) Ts[threadIdx.x * NB + threadIdx.x] = taus[threadIdx.x];
-  __syncthreads();
-  for (int c = 1; c < nbp; ++c) {
-    double2 p = make_double2(0.0, 0.0);
-    for (int l = w; l < c; l += CL_WARPS)
-      if (l >= k) p = cadd(p, cmul(Ts[k * NB + l], Z[c * NB + l]));
-    red[w * NB + k] = p;
+  // recursive doubling instead of 31 dependent column steps: the T of two
+  // adjacent reflector blocks B1, B2 is [[T11, T12], [0, T22]] with
+  // T12 = -T11 (V1^H V2) T22; five levels of two small products each
+  double2* P = red;  // [16 pairs x b x b] <= 256 entries
+  for (int b = 1; b < NB; b <<= 1) {
+    const int bb = b * b, nout = (NB / (2 * b)) * bb;
+    for (int e = threadIdx.x; e < nout; e += CL_THREADS) {  // P = M[B1, B2] T22
+      const int q = e / bb, r = (e % bb) / b, c = e % b, s0 = 2 * b * q;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int l = 0; l <= c; ++l)
+        acc = cadd(acc, cmul(Z[(s0 + b + l) * NB + s0 + r], Ts[(s0 + b + l) * NB + s0 + b + c]));
+      P[e] = acc;
+    }
     __syncthreads();
-    if (w == 0 && k < c) {
-      double2 s = red[k];
-#pragma unroll
-      for (int ww = 1; ww < CL_WARPS; ++ww) s = cadd(s, red[ww * NB + k]);
-      Ts[k * NB + c] = s;
+    for (int e = threadIdx.x; e < nout; e += CL_THREADS) {  // T12 = -T11 P
+      const int q = e / bb, r = (e % bb) / b, c = e % b, s0 = 2 * b * q;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int l = r; l < b; ++l) acc = cadd(acc, cmul(Ts[(s0 + r) * NB + s0 + l], P[q * bb + l * b + c]));
+      Ts[(s0 + r) * NB + s0 + b + c] = make_double2(-acc.x, -acc.y);
     }
     __syncthreads();
   }
