@@ -399,6 +399,147 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp, cudaStream_t s
   QT_LAUNCHED();
 }
 
+// C <- H_p^H C for a WIDE C (the theta side of the QR pair), split by
+// columns: CTA b owns columns [b*CB, b*CB + CB) over all mp rows, so no
+// cross-CTA reduction is needed.  Pass 1 streams V (mp x 32) and the C block
+// through shared memory in double-buffered 128-row chunks and forms
+// W = V^H C_blk on the FP64 tensor pipe; W2 = T^H W; pass 2 re-streams the
+// chunks and writes C_blk -= V W2.  With yh != nullptr the first nbp rows of
+// the result (final rows of Q_full^H theta) are also written, gauge-phased
+// and conjugate-transposed, as the matching block of Y^H (the extraction).
+constexpr int AC_CB = 16;    // columns per CTA
+constexpr int AC_RC = 128;   // rows per chunk
+constexpr int AC_THREADS = 256;
+
+__global__ void __launch_bounds__(AC_THREADS, 1)
+    apply_cols_kernel(const double2* __restrict__ V, long long ldv, const double2* __restrict__ T, int nbp,
+                      double2* C, long long ldc, long long mp, long long nc, const double2* __restrict__ xa,
+                      long long lda, double2* yh, long long ldy) {
+  extern __shared__ __align__(16) double2 acs[];
+  double2* Vb[2] = {acs, acs + AC_RC * NB};                                  // [RC][32] swizzled
+  double2* Cb[2] = {acs + 2 * AC_RC * NB, acs + 2 * AC_RC * NB + AC_RC * AC_CB};  // [RC][CB] swizzled
+  double2* Ws = acs + 2 * AC_RC * NB + 2 * AC_RC * AC_CB;                    // [32][CB]
+  double2* Tp = Ws + NB * AC_CB;                                             // [32][32] T^H
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const long long c0 = static_cast<long long>(blockIdx.x) * AC_CB;
+  const int ncl = static_cast<int>(min(static_cast<long long>(AC_CB), nc - c0));
+  const int nchunk = static_cast<int>((mp + AC_RC - 1) / AC_RC);
+  auto stage = [&](int ch, int buf) {
+    const long long r0 = static_cast<long long>(ch) * AC_RC;
+    for (int e = tid; e < AC_RC * NB; e += AC_THREADS) {
+      const int r = e / NB, c = e % NB;
+      const bool ok = r0 + r < mp;
+      lb_cp16(&Vb[buf][r * NB + lb_sw(r, c)], ok ? &V[(r0 + r) * ldv + c] : V, ok);
+    }
+    for (int e = tid; e < AC_RC * AC_CB; e += AC_THREADS) {
+      const int r = e / AC_CB, c = e % AC_CB;
+      const bool ok = r0 + r < mp && c < ncl;
+      lb_cp16(&Cb[buf][r * AC_CB + lb_sw(r, c)], ok ? &C[(r0 + r) * ldc + c0 + c] : C, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int e = tid; e < NB * NB; e += AC_THREADS) {
+    const int i = e / NB, k = e % NB;
+    Tp[e] = (i < nbp && k < nbp) ? cconj(T[k * NB + i]) : make_double2(0.0, 0.0);
+  }
+  // ---- pass 1: W = V^H C_blk; warp w owns the 8 x 8 block (w / 2, w % 2)
+  const int ib = w >> 1, cb = w & 1;
+  double cre[2] = {0.0, 0.0}, cim[2] = {0.0, 0.0};
+  stage(0, 0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunk) {
+      stage(ch + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < AC_RC; r += 4) {
+      const int rr = r + t;
+      cmma(cre, cim, cconj(Vb[buf][rr * NB + lb_sw(rr, ib * 8 + g)]), Cb[buf][rr * AC_CB + lb_sw(rr, cb * 8 + g)]);
+    }
+    __syncthreads();  // buffer free for the chunk after next
+  }
+#pragma unroll
+  for (int e2 = 0; e2 < 2; ++e2) Ws[(ib * 8 + g) * AC_CB + cb * 8 + 2 * t + e2] = make_double2(cre[e2], cim[e2]);
+  __syncthreads();
+  // ---- W2 = T^H W (same block ownership), kept in registers as B fragments later
+  {
+    double xre[2] = {0.0, 0.0}, xim[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k0 = 0; k0 < NB; k0 += 4)
+      cmma(xre, xim, Tp[(ib * 8 + g) * NB + k0 + t], Ws[(k0 + t) * AC_CB + cb * 8 + g]);
+    __syncthreads();
+#pragma unroll
+    for (int e2 = 0; e2 < 2; ++e2) Ws[(ib * 8 + g) * AC_CB + cb * 8 + 2 * t + e2] = make_double2(xre[e2], xim[e2]);
+  }
+  __syncthreads();
+  // ---- pass 2: C_blk -= V W2, chunk by chunk (16 x 2 blocks of 8 x 8 per chunk)
+  stage(0, 0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunk) {
+      stage(ch + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const long long r0 = static_cast<long long>(ch) * AC_RC;
+    for (int blk = w; blk < (AC_RC / 8) * (AC_CB / 8); blk += AC_THREADS / 32) {
+      const int rb = blk / (AC_CB / 8), bcb = blk % (AC_CB / 8), row = rb * 8 + g;
+      double ure[2], uim[2];
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const double2 c = Cb[buf][row * AC_CB + lb_sw(row, bcb * 8 + 2 * t + e2)];
+        ure[e2] = c.x;
+        uim[e2] = c.y;
+      }
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const double2 av = Vb[buf][row * NB + lb_sw(row, k0 + t)];
+        cmma(ure, uim, make_double2(-av.x, -av.y), Ws[(k0 + t) * AC_CB + bcb * 8 + g]);
+      }
+      const long long gr = r0 + row;
+      if (gr < mp)
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int col = bcb * 8 + 2 * t + e2;
+          if (col < ncl) {
+            const double2 v = make_double2(ure[e2], uim[e2]);
+            C[gr * ldc + c0 + col] = v;
+            if (yh && gr < nbp) {  // extraction: yh[c, i] = ph_i conj(v), ph_i = R_ii / |R_ii|
+              const double2 dg = xa[gr * lda + gr];
+              const double ad = hypot(dg.x, dg.y);
+              const double2 ph = ad == 0.0 ? make_double2(1.0, 0.0) : make_double2(dg.x / ad, dg.y / ad);
+              yh[(c0 + col) * ldy + gr] = cmul(ph, cconj(v));
+            }
+          }
+        }
+    }
+    __syncthreads();
+  }
+}
+
+constexpr size_t apply_cols_smem() {
+  return (size_t(2) * AC_RC * NB + size_t(2) * AC_RC * AC_CB + NB * AC_CB + NB * NB) * sizeof(double2);
+}
+
+void apply_cols(const double2* Vp, long long ldv, const double2* Tp, int nbp, double2* C, long long ldc, long long mp,
+                long long nc, const double2* xa, long long lda, double2* yh, long long ldy, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    QT_CUDA(cudaFuncSetAttribute(apply_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(apply_cols_smem())));
+    attr = true;
+  }
+  apply_cols_kernel<<<static_cast<unsigned>(ceil_div(nc, AC_CB)), AC_THREADS, apply_cols_smem(), st>>>(
+      Vp, ldv, Tp, nbp, C, ldc, mp, nc, xa, lda, yh, ldy);
+  QT_LAUNCHED();
+}
+
 // C <- H_p^H C = C - V T^H (V^H C) on stream st (three DMMA GEMMs; W/W2 and the
 // split-K scratch belong to that stream)
 void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, double2* C, long long ldc,
@@ -742,13 +883,24 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     // ---- theta side: C <- H_p^H C, then rows [j, j + nbp) of C are final
     QT_CUDA(cudaEventRecord(e.event(P0 + p), sx));
     QT_CUDA(cudaStreamWaitEvent(sa, e.event(P0 + p), 0));
-    // rows [j, j + nbp) of H_p^H C are final first: publish them as block p of
-    // Y^H before the rest of C is updated
-    apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa, [&] {
-      extract(j, nbp, sa);
+    // QT_APPLY_COLS=1: one column-split launch (apply_cols_kernel) applies H_p^H
+    // to C and writes block p of Y^H; measured slower at C2 (194 vs 200
+    // steps/s: 80 CTAs each re-streaming all of V hold 80 SMs for ~90 us and
+    // delay both panel chains), so the three-GEMM application is the default
+    static const bool cols_apply = std::getenv("QT_APPLY_COLS") != nullptr;
+    if (cols_apply) {
+      apply_cols(pa.V, kp, pa.T, nbp, c + j * nc, nc, m - j, nc, x + j * k + j, k, yh + j, k, sa);
       stamp("extract" + std::to_string(p), sa);
       QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
-    });
+    } else {
+      // rows [j, j + nbp) of H_p^H C are final first: publish them as block p
+      // of Y^H before the rest of C is updated
+      apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa, [&] {
+        extract(j, nbp, sa);
+        stamp("extract" + std::to_string(p), sa);
+        QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
+      });
+    }
     // ---- X trailing update (look-ahead: next panel's columns on sx, the rest on sxw)
     const long long ntr = k - j - nbp;
     if (fused && ntr > 0) {
