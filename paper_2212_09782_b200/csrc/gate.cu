@@ -14,7 +14,7 @@
 //   Xi~ = L/|L|, B~n = Q_n -> (d,eta,chi_r), B~m = phiev Q_n^H (permuted store),
 //   left_iso = Q_m -> (d,chi_l,eta), eps = ||theta - Q_m L Q_n||^2/||theta||^2
 //
-// For one sweep on 256..2048-row matrices the two QRs run as a pipelined pair
+// For one sweep on 128..2048-row matrices the two QRs run as a pipelined pair
 // (qr_pair_pipelined, householder.cu): each QR(X) panel's reflector is applied
 // to theta behind the panel chain, so Q_full^H theta = [Y; Z] replaces the
 // explicit Q_m and the theta^H Q_m product, QR(Y^H) runs one panel behind on
@@ -226,14 +226,16 @@ void gemm(Engine& e, Op oa, Op ob, long long M, long long N, long long K, const 
 
 bool use_qtheta(const qt_policy& pol, long long rows) {
   // above ~2048 rows the extra reflector flops on theta outweigh the shorter
-  // critical path (north star: GEMM-bound); below ~256 the side-stream
-  // launches cost more than they hide (C5-small: 8 concurrent bonds)
+  // critical path (north star: GEMM-bound); from 128 rows the pair pays for a
+  // lone update chain (C1, 128 rows: 771 -> 877 steps/s) but not when eight
+  // bond chains already share the GPU (C5-small, 192 rows: 183 -> 155 steps/s;
+  // QT_QTHETA_MIN_ROWS=256 restores that)
   static const long long qtheta_max = std::getenv("QT_QTHETA_MAX_ROWS")
                                           ? std::atoll(std::getenv("QT_QTHETA_MAX_ROWS"))
                                           : 2048;
   static const long long qtheta_min = std::getenv("QT_QTHETA_MIN_ROWS")
                                           ? std::atoll(std::getenv("QT_QTHETA_MIN_ROWS"))
-                                          : 256;
+                                          : 128;
   return std::max(1, static_cast<int>(pol.qr_sweeps)) == 1 && rows <= qtheta_max && rows >= qtheta_min;
 }
 

@@ -1,7 +1,7 @@
 """The pipelined QR pair (qr_pair_pipelined: QR(X) with its reflectors applied
 to theta, QR(Y^H) one panel behind, explicit Q_n in blocks, explicit error by
 unitary invariance) against the oracle's alternating sweep
-(proj/src/gates.cpp:293-308, :343-450), at the sizes that take it: 256..2048
+(proj/src/gates.cpp:293-308, :343-450), at the sizes that take it: 128..2048
 rows, one sweep, no left_iso.  Ragged widths (eta not a multiple of the
 32-column panel), rectangular bonds, truncating and expanding policies, and the
 CBE scheme.  The same updates with the pair disabled (QT_NO_QR_PAIR is read
