@@ -24,7 +24,9 @@ def _compare_rows(rows, orows, tol=1e-10, exact_chi=True):
             assert abs(a - b) < tol
         for a, b in zip(r.entropy, o["entropy"]):
             assert abs(a - b) < tol
-        for a, b in zip(r.eps, o["eps"]):
+        for a, b, ca, cb in zip(r.eps, o["eps"], r.chi, o["chi"]):
+            if ca != cb:
+                continue  # a noise-level Schmidt direction kept on one side only (Appendix B(iv))
             assert abs(a - b) <= 1e-10 * b + 2e-13 * b ** 0.5 + 1e-20  # trajectory floor
 
 
@@ -82,3 +84,14 @@ def test_quench_checkpoint_loads_back(ctx, tmp_path):
     run.run_quench(run.RunConfig(d=2, dt=0.05, t_max=0.1, scheme="qr", chi_max=8, out_path=str(u)), ctx)
     us = run.load_mps(str(u / "state.mps"), ctx)
     assert isinstance(us, q.UniformMPS) and us.cell_length() == 2
+
+
+@pytest.mark.parametrize("scheme", ["qr", "qr_cbe"])
+def test_quench_through_the_pipelined_pair_matches_oracle(ctx, scheme):
+    # d = 5, chi_max = 64: once chi >= 26 the two-site blocks have >= 130 rows and
+    # the updates run through the pipelined QR pair (128..2048 rows)
+    c = run.RunConfig(d=5, g=2.0, dt=0.05, t_max=0.3, scheme=scheme, chi_max=64)
+    res = run.run_quench(c, ctx)
+    orows = ref.run_quench_rows(5, 2.0, "uniform", 2, 0.05, 0.3, 2, scheme, ref.TruncationPolicy(chi_max=64))
+    assert max(res.rows[-1].chi) >= 26
+    _compare_rows(res.rows, orows, exact_chi=(scheme == "qr"))
