@@ -103,6 +103,12 @@ qt_status qt_ctx_create(int device, void* stream, qt_ctx** out);
 qt_status qt_ctx_destroy(qt_ctx* ctx);
 qt_status qt_ctx_synchronize(qt_ctx* ctx);
 void* qt_ctx_stream(qt_ctx* ctx);
+/* Performance knob: the smallest two-site block height (d * chi_left rows)
+ * whose update takes the pipelined QR pair on this context (default 128;
+ * rows < 0 restores the default).  Contexts that run concurrently with
+ * other contexts (sharded chains) set 256: there the pair's side streams
+ * cost more than they hide.  Results agree with the other path to rounding. */
+qt_status qt_ctx_set_qr_pair_min_rows(qt_ctx* ctx, int64_t rows);
 
 /* ---- device tensors (ComplexTensor, tensor.hpp:18-61) --------------------- */
 qt_status qt_tensor_create(qt_ctx* ctx, int rank, const uint64_t* shape, qt_tensor** out);

@@ -79,6 +79,7 @@ SIGNATURES = {
     "qt_ctx_destroy": (C.c_int, [P]),
     "qt_ctx_synchronize": (C.c_int, [P]),
     "qt_ctx_stream": (P, [P]),
+    "qt_ctx_set_qr_pair_min_rows": (C.c_int, [P, C.c_int64]),
     "qt_tensor_create": (C.c_int, [P, C.c_int, U64P, PP]),
     "qt_tensor_wrap": (C.c_int, [P, C.c_int, U64P, P, PP]),
     "qt_tensor_free": (C.c_int, [P]),

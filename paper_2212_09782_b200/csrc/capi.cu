@@ -256,6 +256,13 @@ qt_status qt_ctx_synchronize(qt_ctx* ctx) {
 
 void* qt_ctx_stream(qt_ctx* ctx) { return ctx ? static_cast<void*>(ctx->eng.stream) : nullptr; }
 
+qt_status qt_ctx_set_qr_pair_min_rows(qt_ctx* ctx, int64_t rows) {
+  return guard([&] {
+    require(ctx != nullptr, qt::Err::input, "qt_ctx_set_qr_pair_min_rows: null context");
+    ctx->eng.qr_pair_min_rows = rows < 0 ? -1 : rows;
+  });
+}
+
 qt_status qt_tensor_create(qt_ctx* ctx, int rank, const uint64_t* shape, qt_tensor** out) {
   return guard([&] {
     require(ctx && out && (rank == 0 || shape), qt::Err::input, "qt_tensor_create: null argument");

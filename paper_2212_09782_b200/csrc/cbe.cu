@@ -88,7 +88,7 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
   const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
   // Y = Q_m^H theta through the reflectors of QR(X) (see gate_qr_async); theta
   // becomes Q_full^H theta, Q_m is never formed (CBE keeps no left_iso)
-  const bool qtheta = use_qtheta(pol, rows);
+  const bool qtheta = use_qtheta(e, pol, rows);
   for (int it = 0; it < sweeps; ++it) {
     if (it == 0)
       gemm2(e, Op::N, Op::H, rows, eta, cols, theta, cols, theta, cols, X, eta);

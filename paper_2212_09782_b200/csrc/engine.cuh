@@ -94,6 +94,10 @@ struct Engine {
   cudaStream_t side5 = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t event(size_t i);
+  // smallest two-site block height that takes the pipelined QR pair on this
+  // engine (-1: the library default); contexts that run side by side with
+  // other contexts (sharded chains) raise it (qt_ctx_set_qr_pair_min_rows)
+  long long qr_pair_min_rows = -1;
 
   void init(int dev, cudaStream_t st);
   void destroy();

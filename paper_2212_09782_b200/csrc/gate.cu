@@ -224,7 +224,7 @@ void gemm(Engine& e, Op oa, Op ob, long long M, long long N, long long K, const 
 
 }  // namespace
 
-bool use_qtheta(const qt_policy& pol, long long rows) {
+bool use_qtheta(const Engine& e, const qt_policy& pol, long long rows) {
   // above ~2048 rows the extra reflector flops on theta outweigh the shorter
   // critical path (north star: GEMM-bound); from 128 rows the pair pays for a
   // lone update chain (C1, 128 rows: 771 -> 877 steps/s) but not when eight
@@ -236,7 +236,8 @@ bool use_qtheta(const qt_policy& pol, long long rows) {
   static const long long qtheta_min = std::getenv("QT_QTHETA_MIN_ROWS")
                                           ? std::atoll(std::getenv("QT_QTHETA_MIN_ROWS"))
                                           : 128;
-  return std::max(1, static_cast<int>(pol.qr_sweeps)) == 1 && rows <= qtheta_max && rows >= qtheta_min;
+  const long long min_rows = e.qr_pair_min_rows >= 0 ? e.qr_pair_min_rows : qtheta_min;
+  return std::max(1, static_cast<int>(pol.qr_sweeps)) == 1 && rows <= qtheta_max && rows >= min_rows;
 }
 
 void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, long long eta, double2* yh,
@@ -316,7 +317,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   int* flag = reinterpret_cast<int*>(e.dscal + SC_TMP3);
   zero_flag_kernel<<<1, 1, 0, e.stream>>>(flag);
   const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
-  const bool qtheta = use_qtheta(pol, rows);
+  const bool qtheta = use_qtheta(e, pol, rows);
   // QT_X_REASSOC=1 (pipelined pair with Y0 = B^n): X = Xi (phiev Y0^H) on the
   // main stream while theta = Xi phiev is formed on the theta stream (first
   // needed by the reflector of X's first panel); ||theta|| = ||Q_full^H theta||

@@ -52,7 +52,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
 
 // Y = Q_m^H theta through the reflectors of QR(X) (QrOpts::capply): used for
 // one sweep on matrices up to QT_QTHETA_MAX_ROWS rows (default 2048)
-bool use_qtheta(const qt_policy& pol, long long rows);
+bool use_qtheta(const Engine& e, const qt_policy& pol, long long rows);
 // Y^H (cols x eta) from Q_full^H theta (rows x cols) with the gauge phases of
 // the factored X (diag of a, ld eta)
 // (rows [ibeg, iend) only, on stream st; iend < 0: all eta rows, st null: e.stream)

@@ -266,6 +266,9 @@ def device_backend(ctx, scheme: str, policy) -> Backend:
     from . import qrtebd as q
 
     pol = policy.to_c() if isinstance(policy, q.TruncationPolicy) else policy
+    # bond updates of a chain run on several contexts at once: small blocks
+    # skip the pipelined QR pair there (qt_ctx_set_qr_pair_min_rows)
+    _capi.check(ctx.lib.qt_ctx_set_qr_pair_min_rows(ctx.h, 256))
 
     def apply(xi, bm, bn, u):
         upd = q.apply_gate(scheme, xi, bm, bn, u, pol, ctx) if scheme == "qr_cbe" else \
