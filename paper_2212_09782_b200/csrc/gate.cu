@@ -254,11 +254,12 @@ bool use_qr_pair(long long rows, long long cols) {
 }
 
 void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, const double2* a, long long eta,
-                  const double2* w, double* out) {
+                  const double2* w, double* out, cudaStream_t st) {
+  if (!st) st = e.stream;
   double* part = e.dbuf(S_QT_PART, kResidBlocks);
-  qtheta_resid_partial_kernel<<<kResidBlocks, 256, 0, e.stream>>>(qt, rows, cols, a, eta, eta, w, part);
+  qtheta_resid_partial_kernel<<<kResidBlocks, 256, 0, st>>>(qt, rows, cols, a, eta, eta, w, part);
   QT_LAUNCHED();
-  sum_final_kernel<<<1, 32, 0, e.stream>>>(part, kResidBlocks, out);
+  sum_final_kernel<<<1, 32, 0, st>>>(part, kResidBlocks, out);
   QT_LAUNCHED();
 }
 
@@ -455,6 +456,23 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     permute(e, Qp, 3, shp, perm, true, out.b_n);
   }
   ustamp("xi_bn");
+  // explicit error of the pair path on e.side, concurrently with the Hastings
+  // product (both only read theta / Q_n / L; joined before returning)
+  static const bool resid_side = std::getenv("QT_RESID_MAIN") == nullptr;
+  const bool fork_resid = pol.compute_explicit_error && qtheta && resid_side && e.side != nullptr;
+  if (fork_resid) {
+    QT_CUDA(cudaEventRecord(e.event(1000), e.stream));
+    QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1000), 0));
+    double2* W = e.cbuf(S_W, eta * cols);
+    GemmDesc gw;
+    gw.M = eta; gw.N = cols; gw.K = eta;
+    gw.opA = Op::H; gw.A = Rp; gw.lda = eta;
+    gw.opB = Op::H; gw.B = Qp; gw.ldb = eta;
+    gw.C = W; gw.ldc = cols;
+    zgemm(gw, e.gemm_scratch2(), e.side);
+    qtheta_resid(e, theta, rows, cols, X, eta, W, e.dscal + SC_RESID, e.side);
+    QT_CUDA(cudaEventRecord(e.event(1001), e.side));
+  }
   if (out.b_m && !hastings_done) {
     // B~m[i,beta,k] = sum_{j,delta} phiev[beta,i,j,delta] conj(B~n[j,k,delta])
     //             = (phiev (cm*d x d*cr) . Qp)[(beta i), k]   (gates.cpp:186-190)
@@ -473,7 +491,9 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     const int perm[3] = {1, 0, 2};
     permute(e, Qm, 3, shp, perm, false, out.left_iso);
   }
-  if (pol.compute_explicit_error && qtheta) {
+  if (fork_resid) {
+    QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(1001), 0));  // join: the report scalars are complete
+  } else if (pol.compute_explicit_error && qtheta) {
     // W = L Q_n = Rp^H Qp^H (eta x cols); ||theta - Q_m W||^2 = ||Y - W||^2 + ||Z||^2
     double2* W = e.cbuf(S_W, eta * cols);
     gemm(e, Op::H, Op::H, eta, cols, eta, Rp, eta, Qp, eta, W, cols);

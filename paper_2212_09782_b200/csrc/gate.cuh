@@ -63,7 +63,7 @@ void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, l
 bool use_qr_pair(long long rows, long long cols);
 // *out = ||Y - W||^2 + ||Z||^2 = ||theta - Q_m W||^2 (W: eta x cols), fixed-order reduction
 void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, const double2* a, long long eta,
-                  const double2* w, double* out);
+                  const double2* w, double* out, cudaStream_t st = nullptr);
 
 // Collects the report of the last gate_qr_async / CBE update (synchronizes).
 HostReport read_report(Engine& e);
