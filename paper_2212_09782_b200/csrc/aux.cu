@@ -284,7 +284,8 @@ int grid_for(long long total, int per = 256) {
 }  // namespace
 
 void permute(Engine& e, const double2* in, int rank, const long long* shape, const int* perm, bool conj,
-             double2* out, double scale, const double* dscale) {
+             double2* out, double scale, const double* dscale, cudaStream_t st) {
+  if (!st) st = e.stream;
   if (rank < 1 || rank > 4) throw Error(Err::shape, "permute: rank must be 1..4");
   long long in_strides[4];
   long long s = 1;
@@ -303,7 +304,7 @@ void permute(Engine& e, const double2* in, int rank, const long long* shape, con
     const long long batch = total / (R * C);
     dim3 grid(static_cast<unsigned>(ceil_div(C, 32)), static_cast<unsigned>(ceil_div(R, 32)),
               static_cast<unsigned>(batch));
-    transpose_tiled_kernel<<<grid, dim3(32, 8), 0, e.stream>>>(in, R, C, conj, out);
+    transpose_tiled_kernel<<<grid, dim3(32, 8), 0, st>>>(in, R, C, conj, out);
     QT_LAUNCHED();
     return;
   }
@@ -313,7 +314,7 @@ void permute(Engine& e, const double2* in, int rank, const long long* shape, con
     p.out_shape[k] = shape[perm[k]];
     p.in_stride_for_out[k] = in_strides[perm[k]];
   }
-  permute_kernel<<<grid_for(total), 256, 0, e.stream>>>(in, p, total, conj, scale, dscale, out);
+  permute_kernel<<<grid_for(total), 256, 0, st>>>(in, p, total, conj, scale, dscale, out);
   QT_LAUNCHED();
 }
 

@@ -113,7 +113,7 @@ struct Engine {
 // ---- kernels shared by the modules (aux.cu) -------------------------------
 // out = scale * [conj](permute(in)); rank <= 4, perm[k] = input axis of output axis k
 void permute(Engine& e, const double2* in, int rank, const long long* shape, const int* perm, bool conj,
-             double2* out, double scale = 1.0, const double* dscale = nullptr);
+             double2* out, double scale = 1.0, const double* dscale = nullptr, cudaStream_t st = nullptr);
 // out[0] = sum |x|^2 over a (rows x cols, ld) matrix, deterministic
 void norm2(Engine& e, const double2* x, long long rows, long long cols, long long ld, double* out);
 // dst = src over rows x cols blocks with leading dimensions

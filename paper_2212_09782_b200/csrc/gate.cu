@@ -443,26 +443,31 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   norm2(e, Rp, eta, eta, eta, e.dscal + SC_L2);
   inv_norm_kernel<<<1, 1, 0, e.stream>>>(e.dscal, SC_THETA2, SC_L2, pol.skip_renormalize ? 1 : 0, SC_TMP0);
   QT_LAUNCHED();
+  // pair path: the output permutes and the explicit-error products run on
+  // e.side, concurrently with the Hastings product on the main stream (they
+  // only read L, Q_n and Q_full^H theta; joined before returning)
+  static const bool resid_side = std::getenv("QT_RESID_MAIN") == nullptr;
+  const bool fork_tail = qtheta && resid_side && e.side != nullptr;
+  const cudaStream_t tail_st = fork_tail ? e.side : e.stream;
+  if (fork_tail) {
+    QT_CUDA(cudaEventRecord(e.event(1000), e.stream));
+    QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1000), 0));
+  }
   {
     // Xi~ = L / den = Rp^H / den   (gates.cpp:365-370)
     const long long shp[2] = {eta, eta};
     const int perm[2] = {1, 0};
-    permute(e, Rp, 2, shp, perm, true, out.xi, 1.0, e.dscal + SC_TMP0);
+    permute(e, Rp, 2, shp, perm, true, out.xi, 1.0, e.dscal + SC_TMP0, tail_st);
   }
   {
     // B~n[j,k,delta] = Q_n[k,(j delta)] = conj(Qp[(j delta),k])   (gates.cpp:193-196)
     const long long shp[3] = {d, cr, eta};
     const int perm[3] = {0, 2, 1};
-    permute(e, Qp, 3, shp, perm, true, out.b_n);
+    permute(e, Qp, 3, shp, perm, true, out.b_n, 1.0, nullptr, tail_st);
   }
   ustamp("xi_bn");
-  // explicit error of the pair path on e.side, concurrently with the Hastings
-  // product (both only read theta / Q_n / L; joined before returning)
-  static const bool resid_side = std::getenv("QT_RESID_MAIN") == nullptr;
-  const bool fork_resid = pol.compute_explicit_error && qtheta && resid_side && e.side != nullptr;
+  const bool fork_resid = fork_tail && pol.compute_explicit_error;
   if (fork_resid) {
-    QT_CUDA(cudaEventRecord(e.event(1000), e.stream));
-    QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1000), 0));
     double2* W = e.cbuf(S_W, eta * cols);
     GemmDesc gw;
     gw.M = eta; gw.N = cols; gw.K = eta;
@@ -491,8 +496,9 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     const int perm[3] = {1, 0, 2};
     permute(e, Qm, 3, shp, perm, false, out.left_iso);
   }
-  if (fork_resid) {
-    QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(1001), 0));  // join: the report scalars are complete
+  if (fork_tail && !fork_resid) QT_CUDA(cudaEventRecord(e.event(1001), e.side));
+  if (fork_tail) {
+    QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(1001), 0));  // join: outputs and report scalars complete
   } else if (pol.compute_explicit_error && qtheta) {
     // W = L Q_n = Rp^H Qp^H (eta x cols); ||theta - Q_m W||^2 = ||Y - W||^2 + ||Z||^2
     double2* W = e.cbuf(S_W, eta * cols);
