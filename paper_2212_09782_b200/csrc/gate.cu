@@ -327,6 +327,17 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   static const bool reassoc = std::getenv("QT_X_REASSOC") != nullptr;
   const bool pair = qtheta && !out.left_iso && use_qr_pair(rows, cols);
   const bool x_reassoc = reassoc && pair && eta == cn && sweeps == 1;
+  // Y0 = B^n regrouped (gates.cpp:357-361) on e.side while theta is built
+  const bool y0_early = (eta == cn) && e.side != nullptr;
+  if (y0_early) {
+    double2* y = e.cbuf(S_Y0, cn * cols);
+    QT_CUDA(cudaEventRecord(e.event(1002), e.stream));
+    QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1002), 0));
+    const long long shp[3] = {d, cn, cr};
+    const int perm[3] = {1, 0, 2};
+    permute(e, bn, 3, shp, perm, false, y, 1.0, nullptr, e.side);
+    QT_CUDA(cudaEventRecord(e.event(1003), e.side));
+  }
   build_theta(e, D, xi, bm, bn, u, SC_THETA2, x_reassoc);
   ustamp("theta");
   double2* phiev = e.cbuf(S_PHIEV, cm * d * d * cr);
@@ -342,7 +353,10 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   // initial guess, gates.cpp:357-361
   const bool y0_is_bn = (eta == cn);
   const double2* y0 = theta;  // first eta rows of the grouped theta
-  if (y0_is_bn) {
+  if (y0_is_bn && y0_early) {
+    y0 = e.cbuf(S_Y0, cn * cols);
+    QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(1003), 0));
+  } else if (y0_is_bn) {
     double2* y = e.cbuf(S_Y0, cn * cols);
     const long long shp[3] = {d, cn, cr};
     const int perm[3] = {1, 0, 2};
