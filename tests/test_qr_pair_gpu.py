@@ -134,3 +134,23 @@ def test_pair_concurrent_cell_L4_matches_oracle(ctx):
         sd = q.schmidt_values(snap, m, ctx)
         so = ref.schmidt_values(st, m)
         assert np.max(np.abs(sd[: len(so)] - so)[so >= 1e-6 * so[0]]) <= 1e-10 * so[0]
+
+
+def test_pair_and_sequential_paths_agree_per_context_knob():
+    # qt_ctx_set_qr_pair_min_rows switches one context to the sequential
+    # QR(X) -> theta^H Q_m -> QR(Y^H) path: the two paths agree to rounding
+    from paper_2212_09782_b200._capi import Context, check
+    d, chi = 5, 64
+    xi, bm, bn = random_inputs(d, chi, seed=321)
+    gate = model.make_gate(model.bond_hamiltonian(d, 2.0), 0.05)
+    kw = dict(chi_max=chi, sv_cutoff=1e-14, delta_chi_abs=0, delta_chi_rel=0.0)
+    outs = []
+    for min_rows in (-1, 1 << 20):
+        with Context(0) as c:
+            check(c.lib.qt_ctx_set_qr_pair_min_rows(c.h, min_rows))
+            u = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**kw), c, want_left_iso=False)
+            outs.append((u.b_m.numpy(), u.xi_n.numpy(), u.b_n.numpy(), u.report.eps_trunc))
+    (bm1, x1, bn1, e1), (bm2, x2, bn2, e2) = outs
+    assert np.allclose(x1, x2, atol=1e-12) and np.allclose(bn1, bn2, atol=1e-11)
+    assert np.allclose(bm1, bm2, atol=1e-11)
+    assert abs(e1 - e2) <= 1e-10 * e2 + 1e-20
