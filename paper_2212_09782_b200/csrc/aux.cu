@@ -276,6 +276,18 @@ __global__ void finite_kernel(const double2* __restrict__ x, long long n, int* f
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+__global__ void finite2d_kernel(const double2* __restrict__ x, long long rows, long long cols, long long ld,
+                                int* flag) {
+  bool bad = false;
+  const long long n = rows * cols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double2 v = x[(e / cols) * ld + e % cols];
+    bad |= !isfinite(v.x) || !isfinite(v.y);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 int grid_for(long long total, int per = 256) {
   const long long b = ceil_div(total, per);
   return static_cast<int>(b < 16LL * kNumSMs ? (b > 0 ? b : 1) : 16LL * kNumSMs);
@@ -342,6 +354,13 @@ void set_identity(Engine& e, double2* q, long long rows, long long cols, long lo
 void check_finite(Engine& e, const double2* x, long long n, int* dflag) {
   if (n == 0) return;
   finite_kernel<<<grid_for(n), 256, 0, e.stream>>>(x, n, dflag);
+  QT_LAUNCHED();
+}
+
+void check_finite_2d(Engine& e, const double2* x, long long rows, long long cols, long long ld, int* dflag,
+                     cudaStream_t st) {
+  if (rows * cols == 0) return;
+  finite2d_kernel<<<grid_for(rows * cols), 256, 0, st ? st : e.stream>>>(x, rows, cols, ld, dflag);
   QT_LAUNCHED();
 }
 

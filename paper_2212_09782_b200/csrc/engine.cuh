@@ -121,6 +121,9 @@ void copy2d(Engine& e, const double2* src, long long lds, double2* dst, long lon
             long long cols);
 void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld, cudaStream_t st = nullptr);
 void check_finite(Engine& e, const double2* x, long long n, int* dflag);
+// the same over a (rows x cols, ld) block, on `st` (nullptr: e.stream)
+void check_finite_2d(Engine& e, const double2* x, long long rows, long long cols, long long ld, int* dflag,
+                     cudaStream_t st = nullptr);
 
 // ---- Householder QR (householder.cu) ----------------------------------------
 // Blocked Householder QR of the m x n row-major matrix a (ld lda), factored

@@ -385,14 +385,47 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     gemm(e, Op::N, Op::H, cm * d, eta, cols, phiev, cols, y0, cols, P, eta);
     gemm(e, Op::N, Op::N, cl, d * eta, cm, xi, cm, P, d * eta, X, d * eta);
   }
+  // pipelined pair: X = theta Y0^H in two column blocks -- the columns of the
+  // first two panels on the main stream, the rest on e.side concurrently with
+  // panel 0 (e.side carries the pair's wide look-ahead updates, the first
+  // work to touch those columns, so stream order covers the dependency);
+  // QT_NO_X_SPLIT=1 forms X in one GEMM
+  static const bool x_split_env = std::getenv("QT_NO_X_SPLIT") == nullptr;
+  const long long x_head = 64;
+  const bool x_split = x_split_env && pair && !x_reassoc && e.side != nullptr && eta > x_head + 32;
   for (int it = 0; it < sweeps; ++it) {
-    if (it == 0 && x_reassoc)
-      ;  // X formed above
-    else if (it == 0)
-      gemm(e, Op::N, Op::H, rows, eta, cols, theta, cols, y0, cols, X, eta);  // X = theta Y0^H
-    else
-      gemm(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);   // Y0 = Q_n = Qp^H
-    check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
+    const double2* xb = it == 0 ? y0 : Qp;  // X = theta xb^H (it = 0) / theta xb (Y0 = Q_n = Qp^H)
+    if (it == 0 && x_reassoc) {
+      // X formed above
+    } else if (x_split) {
+      QT_CUDA(cudaEventRecord(e.event(1004), e.stream));
+      QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1004), 0));
+      GemmScratch gss;
+      gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
+      gss.partial_elems = size_t(1) << 22;
+      gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
+      gss.tile_sums_elems = size_t(1) << 16;
+      GemmDesc g;
+      g.M = rows; g.N = eta - x_head; g.K = cols;
+      g.A = theta; g.lda = cols;
+      g.opB = it == 0 ? Op::H : Op::N;
+      g.B = it == 0 ? xb + x_head * cols : xb + x_head;
+      g.ldb = it == 0 ? cols : eta;
+      g.C = X + x_head; g.ldc = eta;
+      zgemm(g, gss, e.side);
+      check_finite_2d(e, X + x_head, rows, eta - x_head, eta, flag, e.side);
+      if (it == 0)
+        gemm(e, Op::N, Op::H, rows, x_head, cols, theta, cols, xb, cols, X, eta);
+      else
+        gemm(e, Op::N, Op::N, rows, x_head, cols, theta, cols, xb, eta, X, eta);
+      check_finite_2d(e, X, rows, x_head, eta, flag);
+    } else {
+      if (it == 0)
+        gemm(e, Op::N, Op::H, rows, eta, cols, theta, cols, xb, cols, X, eta);  // X = theta Y0^H
+      else
+        gemm(e, Op::N, Op::N, rows, eta, cols, theta, cols, xb, eta, X, eta);   // Y0 = Q_n = Qp^H
+    }
+    if (!x_split) check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
     ustamp("X");
     if (qtheta && !out.left_iso && use_qr_pair(rows, cols)) {
       // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
