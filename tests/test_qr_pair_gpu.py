@@ -154,3 +154,23 @@ def test_pair_and_sequential_paths_agree_per_context_knob():
     assert np.allclose(x1, x2, atol=1e-12) and np.allclose(bn1, bn2, atol=1e-11)
     assert np.allclose(bm1, bm2, atol=1e-11)
     assert abs(e1 - e2) <= 1e-10 * e2 + 1e-20
+
+
+@pytest.mark.parametrize("where", ["xi", "bn"])
+def test_pair_nonfinite_input_is_input_error(ctx, where):
+    """require_finite_matrix (proj/src/linalg.cpp:17-21) through the pair with X
+    formed in two column blocks (eta = 256 > 96): the NaN reaches X's head
+    columns (main stream) and its remainder (look-ahead stream); the update
+    raises InputError and the context stays usable."""
+    d, chi = 5, 256
+    xi, bm, bn = random_inputs(d, chi, seed=11)
+    gate = model.make_gate(model.bond_hamiltonian(d, 2.0), 0.05)
+    pol = dict(chi_max=chi, sv_cutoff=1e-14, delta_chi_abs=0, delta_chi_rel=0.0)
+    bad = {"xi": xi.copy(), "bn": bn.copy()}
+    bad[where][(3,) * bad[where].ndim] = np.nan
+    args = (bad["xi"], bm, bad["bn"])
+    with pytest.raises(q.InputError):
+        q.apply_gate_qr(*args, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=False)
+    o = ref.apply_gate_qr(xi, bm, bn, gate, ref.TruncationPolicy(**pol))
+    upd = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=False)
+    compare(upd, o, xi)
