@@ -157,6 +157,10 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 bool qr_pair_fits(long long m, long long nc);
 // on_qblock (optional): called on the Q stream once columns [c0, c0 + nb) of
 // qy are formed and gauge-fixed (consumers of Q start behind the Y chain).
+// Callers may leave work in flight on e.side (the X look-ahead stream: X's
+// columns past the first two panels, first touched there by the wide update)
+// and have e.side2 wait for anything that still reads C (C is first written
+// on e.side2).
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
                        double2* qy, double2* ry,
                        const std::function<void(long long, long long, cudaStream_t)>& extract,

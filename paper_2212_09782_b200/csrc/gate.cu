@@ -403,8 +403,12 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
       else
         gemm(e, Op::N, Op::N, rows, x_head, cols, theta, cols, xb, eta, X, eta);
       check_finite_2d(e, X, rows, x_head, eta, flag);
-      // the rest behind the head: issued together, the two GEMMs share the
-      // SMs and the head (panel 0's input) finishes late (208 vs 214 steps/s)
+      // the rest behind the head on e.side (issued together, the two GEMMs
+      // share the SMs and the head, panel 0's input, finishes late: 208 vs 214
+      // steps/s; issued inside the pair behind panel 0 it contends with the
+      // first reflector application instead: 207).  It reads theta, which the
+      // pair overwrites with Q_full^H theta on e.side2 from panel 0 on, so
+      // e.side2 waits for it
       QT_CUDA(cudaEventRecord(e.event(1004), e.stream));
       QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1004), 0));
       GemmScratch gss;
@@ -420,6 +424,8 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
       g.ldb = it == 0 ? cols : eta;
       g.C = X + x_head; g.ldc = eta;
       zgemm(g, gss, e.side);
+      QT_CUDA(cudaEventRecord(e.event(1005), e.side));
+      QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(1005), 0));
       check_finite_2d(e, X + x_head, rows, eta - x_head, eta, flag, e.side);
     } else {
       if (it == 0)
