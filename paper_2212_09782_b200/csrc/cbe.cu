@@ -89,12 +89,17 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
   // Y = Q_m^H theta through the reflectors of QR(X) (see gate_qr_async); theta
   // becomes Q_full^H theta, Q_m is never formed (CBE keeps no left_iso)
   const bool qtheta = use_qtheta(e, pol, rows);
+  const bool x_split = qtheta && use_qr_pair(rows, cols) && x_split_applies(e, eta);
   for (int it = 0; it < sweeps; ++it) {
-    if (it == 0)
-      gemm2(e, Op::N, Op::H, rows, eta, cols, theta, cols, theta, cols, X, eta);
-    else
-      gemm2(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);
-    check_finite(e, X, rows * eta, flag);
+    if (x_split) {
+      x_gemm_split(e, rows, eta, cols, theta, it == 0 ? theta : Qp, it == 0, X, flag);
+    } else {
+      if (it == 0)
+        gemm2(e, Op::N, Op::H, rows, eta, cols, theta, cols, theta, cols, X, eta);
+      else
+        gemm2(e, Op::N, Op::N, rows, eta, cols, theta, cols, Qp, eta, X, eta);
+      check_finite(e, X, rows * eta, flag);
+    }
     if (qtheta && use_qr_pair(rows, cols)) {
       qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp,
                         [&](long long r0, long long nr, cudaStream_t st) {

@@ -248,6 +248,45 @@ void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, l
   QT_LAUNCHED();
 }
 
+bool x_split_applies(const Engine& e, long long eta) {
+  static const bool off = std::getenv("QT_NO_X_SPLIT") != nullptr;
+  return !off && e.side != nullptr && eta > kXHead + 32;
+}
+
+void x_gemm_split(Engine& e, long long rows, long long eta, long long cols, const double2* theta,
+                  const double2* xb, bool xb_h, double2* X, int* flag) {
+  // head: the columns of the first two panels, on the main stream
+  GemmDesc h;
+  h.M = rows; h.N = kXHead; h.K = cols;
+  h.A = theta; h.lda = cols;
+  h.opB = xb_h ? Op::H : Op::N;
+  h.B = xb; h.ldb = xb_h ? cols : eta;
+  h.C = X; h.ldc = eta;
+  zgemm(h, e.gemm_scratch(), e.stream);
+  check_finite_2d(e, X, rows, kXHead, eta, flag);
+  // the rest behind the head on e.side (issued together, the two GEMMs share
+  // the SMs and the head, panel 0's input, finishes late: 208 vs 214 steps/s;
+  // issued inside the pair behind panel 0 it contends with the first
+  // reflector application instead: 207).  It reads theta, which the pair
+  // overwrites with Q_full^H theta on e.side2 from panel 0 on, so e.side2
+  // waits for it
+  QT_CUDA(cudaEventRecord(e.event(1004), e.stream));
+  QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1004), 0));
+  GemmScratch gss;
+  gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
+  gss.partial_elems = size_t(1) << 22;
+  gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
+  gss.tile_sums_elems = size_t(1) << 16;
+  GemmDesc g = h;
+  g.N = eta - kXHead;
+  g.B = xb_h ? xb + kXHead * cols : xb + kXHead;
+  g.C = X + kXHead;
+  zgemm(g, gss, e.side);
+  QT_CUDA(cudaEventRecord(e.event(1005), e.side));
+  QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(1005), 0));
+  check_finite_2d(e, X + kXHead, rows, eta - kXHead, eta, flag, e.side);
+}
+
 bool use_qr_pair(long long rows, long long cols) {
   static const bool off = std::getenv("QT_NO_QR_PAIR") != nullptr;
   return !off && qr_pair_fits(rows, cols);
@@ -385,48 +424,13 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     gemm(e, Op::N, Op::H, cm * d, eta, cols, phiev, cols, y0, cols, P, eta);
     gemm(e, Op::N, Op::N, cl, d * eta, cm, xi, cm, P, d * eta, X, d * eta);
   }
-  // pipelined pair: X = theta Y0^H in two column blocks -- the columns of the
-  // first two panels on the main stream, then the rest on e.side concurrently
-  // with panel 0 (e.side carries the pair's wide look-ahead updates, the first
-  // work to touch those columns, so stream order covers the dependency);
-  // C2 203.6 -> 214 steps/s.  QT_NO_X_SPLIT=1 forms X in one GEMM
-  static const bool x_split_env = std::getenv("QT_NO_X_SPLIT") == nullptr;
-  const long long x_head = 64;
-  const bool x_split = x_split_env && pair && !x_reassoc && e.side != nullptr && eta > x_head + 32;
+  const bool x_split = pair && !x_reassoc && x_split_applies(e, eta);
   for (int it = 0; it < sweeps; ++it) {
     const double2* xb = it == 0 ? y0 : Qp;  // X = theta xb^H (it = 0) / theta xb (Y0 = Q_n = Qp^H)
     if (it == 0 && x_reassoc) {
       // X formed above
     } else if (x_split) {
-      if (it == 0)
-        gemm(e, Op::N, Op::H, rows, x_head, cols, theta, cols, xb, cols, X, eta);
-      else
-        gemm(e, Op::N, Op::N, rows, x_head, cols, theta, cols, xb, eta, X, eta);
-      check_finite_2d(e, X, rows, x_head, eta, flag);
-      // the rest behind the head on e.side (issued together, the two GEMMs
-      // share the SMs and the head, panel 0's input, finishes late: 208 vs 214
-      // steps/s; issued inside the pair behind panel 0 it contends with the
-      // first reflector application instead: 207).  It reads theta, which the
-      // pair overwrites with Q_full^H theta on e.side2 from panel 0 on, so
-      // e.side2 waits for it
-      QT_CUDA(cudaEventRecord(e.event(1004), e.stream));
-      QT_CUDA(cudaStreamWaitEvent(e.side, e.event(1004), 0));
-      GemmScratch gss;
-      gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
-      gss.partial_elems = size_t(1) << 22;
-      gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
-      gss.tile_sums_elems = size_t(1) << 16;
-      GemmDesc g;
-      g.M = rows; g.N = eta - x_head; g.K = cols;
-      g.A = theta; g.lda = cols;
-      g.opB = it == 0 ? Op::H : Op::N;
-      g.B = it == 0 ? xb + x_head * cols : xb + x_head;
-      g.ldb = it == 0 ? cols : eta;
-      g.C = X + x_head; g.ldc = eta;
-      zgemm(g, gss, e.side);
-      QT_CUDA(cudaEventRecord(e.event(1005), e.side));
-      QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(1005), 0));
-      check_finite_2d(e, X + x_head, rows, eta - x_head, eta, flag, e.side);
+      x_gemm_split(e, rows, eta, cols, theta, xb, it == 0, X, flag);
     } else {
       if (it == 0)
         gemm(e, Op::N, Op::H, rows, eta, cols, theta, cols, xb, cols, X, eta);  // X = theta Y0^H

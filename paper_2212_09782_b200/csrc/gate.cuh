@@ -61,6 +61,17 @@ void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, l
 // the two QRs of the sweep run as a pipelined pair (qr_pair_pipelined) when
 // both heights fit one block-reflector cluster (QT_NO_QR_PAIR disables it)
 bool use_qr_pair(long long rows, long long cols);
+// X = theta xb^H (xb_h) or theta xb for the pipelined pair, in two column
+// blocks: the first two panels' kXHead columns on e.stream, the rest on
+// e.side concurrently with panel 0 (e.side carries the pair's wide
+// look-ahead updates, the first work to touch those columns, so stream order
+// is the dependency; e.side2, where the pair first writes theta, waits for
+// it).  Non-finite entries set *flag.  C2: 203 -> 216 steps/s.
+// QT_NO_X_SPLIT=1 forms X in one GEMM.
+constexpr long long kXHead = 64;
+bool x_split_applies(const Engine& e, long long eta);
+void x_gemm_split(Engine& e, long long rows, long long eta, long long cols, const double2* theta,
+                  const double2* xb, bool xb_h, double2* X, int* flag);
 // *out = ||Y - W||^2 + ||Z||^2 = ||theta - Q_m W||^2 (W: eta x cols), fixed-order reduction
 void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, const double2* a, long long eta,
                   const double2* w, double* out, cudaStream_t st = nullptr);
