@@ -248,22 +248,32 @@ void qtheta_yh(Engine& e, const double2* qt, long long cols, const double2* a, l
   QT_LAUNCHED();
 }
 
+long long x_head_cols() {
+  static const long long v = [] {
+    const char* s = std::getenv("QT_X_HEAD");
+    const long long h = s ? std::atoll(s) : kXHead;
+    return h >= 64 && h % 32 == 0 ? h : kXHead;
+  }();
+  return v;
+}
+
 bool x_split_applies(const Engine& e, long long eta) {
   static const bool off = std::getenv("QT_NO_X_SPLIT") != nullptr;
-  return !off && e.side != nullptr && eta > kXHead + 32;
+  return !off && e.side != nullptr && eta > x_head_cols() + 32;
 }
 
 void x_gemm_split(Engine& e, long long rows, long long eta, long long cols, const double2* theta,
                   const double2* xb, bool xb_h, double2* X, int* flag) {
+  const long long xh = x_head_cols();
   // head: the columns of the first two panels, on the main stream
   GemmDesc h;
-  h.M = rows; h.N = kXHead; h.K = cols;
+  h.M = rows; h.N = xh; h.K = cols;
   h.A = theta; h.lda = cols;
   h.opB = xb_h ? Op::H : Op::N;
   h.B = xb; h.ldb = xb_h ? cols : eta;
   h.C = X; h.ldc = eta;
   zgemm(h, e.gemm_scratch(), e.stream);
-  check_finite_2d(e, X, rows, kXHead, eta, flag);
+  check_finite_2d(e, X, rows, xh, eta, flag);
   // the rest behind the head on e.side (issued together, the two GEMMs share
   // the SMs and the head, panel 0's input, finishes late: 208 vs 214 steps/s;
   // issued inside the pair behind panel 0 it contends with the first
@@ -278,13 +288,13 @@ void x_gemm_split(Engine& e, long long rows, long long eta, long long cols, cons
   gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
   gss.tile_sums_elems = size_t(1) << 16;
   GemmDesc g = h;
-  g.N = eta - kXHead;
-  g.B = xb_h ? xb + kXHead * cols : xb + kXHead;
-  g.C = X + kXHead;
+  g.N = eta - xh;
+  g.B = xb_h ? xb + xh * cols : xb + xh;
+  g.C = X + xh;
   zgemm(g, gss, e.side);
   QT_CUDA(cudaEventRecord(e.event(1005), e.side));
   QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(1005), 0));
-  check_finite_2d(e, X + kXHead, rows, eta - kXHead, eta, flag, e.side);
+  check_finite_2d(e, X + xh, rows, eta - xh, eta, flag, e.side);
 }
 
 bool use_qr_pair(long long rows, long long cols) {

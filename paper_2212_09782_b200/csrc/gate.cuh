@@ -69,6 +69,7 @@ bool use_qr_pair(long long rows, long long cols);
 // it).  Non-finite entries set *flag.  C2: 203 -> 216 steps/s.
 // QT_NO_X_SPLIT=1 forms X in one GEMM.
 constexpr long long kXHead = 64;
+long long x_head_cols();  // kXHead, or QT_X_HEAD (a multiple of 32, >= 64; diagnostics)
 bool x_split_applies(const Engine& e, long long eta);
 void x_gemm_split(Engine& e, long long rows, long long eta, long long cols, const double2* theta,
                   const double2* xb, bool xb_h, double2* X, int* flag);
