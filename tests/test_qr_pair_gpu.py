@@ -81,9 +81,10 @@ def test_pair_cbe_update_matches_oracle(ctx, d, chi, dabs):
     assert abs(u.report.eps_trunc - o.report.eps_trunc) <= 1e-10 * o.report.eps_trunc + 1e-20
 
 
-def test_pair_uniform_steps_match_oracle(ctx):
+@pytest.mark.parametrize("chi", [64, 128])  # 128: eta > 96, X formed in two column blocks
+def test_pair_uniform_steps_match_oracle(ctx, chi):
     # a few device-resident C2-shaped steps (graph replay) against the oracle
-    d, chi = 5, 64
+    d = 5
     rng = np.random.default_rng(5)
     sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(2)]
     bonds = []
@@ -109,10 +110,11 @@ def test_pair_uniform_steps_match_oracle(ctx):
         assert abs(zd - zo) < 1e-10
 
 
-def test_pair_concurrent_cell_L4_matches_oracle(ctx):
+@pytest.mark.parametrize("chi", [64, 128])  # 128: each engine splits its X GEMM over two streams
+def test_pair_concurrent_cell_L4_matches_oracle(ctx, chi):
     # L = 4: the two same-parity updates of a layer run on concurrent engines,
     # each with its own six-stream pipelined pair, inside one captured graph
-    d, chi, L = 5, 64, 4
+    d, L = 5, 4
     rng = np.random.default_rng(44)
     sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(L)]
     bonds = []
