@@ -1,27 +1,33 @@
 #!/usr/bin/env python
 """Benchmark of the B200 QR-TEBD bond update (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config north] [--impl ours|reference]
 
-Workload (default, BASELINE.json configs[1] = SURVEY.md C2): global quench of
-the d=5 quantum clock model, uniform MPS with unit cell L=2, chi=256, QR
-truncation (chi_max = chi, so eta = chi), complex128, Trotter order 2
-(3 dependent two-site updates per step), g=2, dt=0.05, explicit truncation
-error on (the quench default, proj/include/qrtebd/gates.hpp:51).  Synthetic
-steady-state input at fixed chi: random right isometries and a Gaussian bond
-matrix (the bench_cell recipe, proj/src/run.cpp:345-381).
+Workload (default at N=1: the north-star configuration of BASELINE.json,
+SURVEY.md §8(d) "North-star target"): global quench of the d=5 quantum clock
+model, uniform MPS with unit cell L=2, chi=1024, QR truncation (chi_max = chi,
+so eta = chi), complex128, Trotter order 2 (3 dependent two-site updates per
+step), g=2, dt=0.05, explicit truncation error on (the quench default,
+proj/include/qrtebd/gates.hpp:51).  Synthetic steady-state input at fixed
+chi: random right isometries and a Gaussian bond matrix (the bench_cell
+recipe, proj/src/run.cpp:345-381).  theta = 419 MB, far larger than L2.
 
-A "step" is one tebd_step (proj/src/gates.cpp:513-540) through the C-ABI
-qt_tebd_step_uniform with the state resident in HBM.  `value` = Trotter
-steps/s; `e2e` = the same metric with the state copied host->device from
-pinned memory before and device->host after every step.  The uniform cell
-does not shard (3 strictly dependent updates): N GPUs run N replicas
-("replicas only"), value = N x per-replica rate from the max time
-over ranks.
+A "step" is one tebd_step (proj/src/gates.cpp:513-540) with the state
+resident in HBM (device-resident UniformMPS, one CUDA-graph replay per
+step).  `value` = Trotter steps/s; `e2e` = the same metric with the state
+copied host->device from pinned memory before and device->host after every
+step; `roofline` = the whole step's algorithmic flops per
+second against the FP64 DMMA peak measured in the run.
 
---impl reference times the reference algorithm on the host CPU (the NumPy/LAPACK
-oracle port, oracle/qrtebd_oracle.py; the C++/Eigen reference cannot be built
-here) on the same config.
+The uniform cell does not shard (3 strictly dependent updates, a single bond
+is never split).  Under torchrun with N > 1 and no --config the default
+workload is the C5 finite chain (BASELINE.json configs[4]: N=256 sites,
+chi=512), sites sharded over the ranks with boundary exchange (strong
+scaling); --config <uniform cell> with N > 1 runs N replicas.
+
+--impl reference times the reference algorithm on the host CPU (the
+NumPy/LAPACK oracle port, oracle/qrtebd_oracle.py) on the
+same config, as a bounded sample of single bond updates.
 """
 from __future__ import annotations
 
@@ -224,47 +230,94 @@ def host_info():
     return info
 
 
-def cpu_reference_rate(cfg, budget_s, min_steps=1, warmup=0, seed=0x51AB):
-    """Reference algorithm on the host cores: the oracle port (test infra)."""
+def cpu_reference_rate(cfg, budget_s, min_updates=1, warmup_updates=0, seed=0x51AB, scheme=None):
+    """Reference algorithm on the host cores (the oracle port: test infra,
+    never the measured product).  Times single bond updates in Trotter order
+    on the evolving L=2 state (even dt/2, odd dt, even dt/2, ...); a Trotter
+    step is exactly 3 updates and nothing else (proj/src/gates.cpp:513-540),
+    so steps/s = (updates / 3) / elapsed.  Bounded sample: stops after
+    `min_updates` once `budget_s` has elapsed (at least one update).
+    Returns (steps/s, updates timed, seconds)."""
     from oracle import qrtebd_oracle as ref
     from paper_2212_09782_b200 import model
-    _, d, chi, scheme, _, _ = cfg
+    _, d, chi, cfg_scheme, _, _ = cfg
+    scheme = scheme or cfg_scheme
     sites, bonds = synthetic_state(d, chi, seed)
-    st = ref.UniformMPS(d, [s.copy() for s in sites], [b.copy() for b in bonds])
-    sched = [(p, model.make_gate(model.bond_hamiltonian(d, 2.0), dte)) for p, dte in model.layer_structure(0.05, 2)]
+    sites, bonds = [x.copy() for x in sites], [x.copy() for x in bonds]
+    gates = [model.make_gate(model.bond_hamiltonian(d, 2.0), dte) for _, dte in model.layer_structure(0.05, 2)]
     pol = ref.TruncationPolicy(**policy_kw(cfg))
-    for _ in range(warmup):
-        st, _ = ref.tebd_step_uniform(st, sched, scheme, pol)
+    k = 0
+
+    def one_update():
+        nonlocal k
+        layer = k % 3
+        m = 0 if layer != 1 else 1  # L = 2: even bond (0,1), odd bond (1,0)
+        n = 1 - m
+        upd = ref.apply_gate(scheme, bonds[m], sites[m], sites[n], gates[layer], pol)
+        sites[m], bonds[n], sites[n] = upd.b_m, upd.xi_n, upd.b_n
+        k += 1
+
+    for _ in range(warmup_updates):
+        one_update()
     n, t0 = 0, time.perf_counter()
-    while n < min_steps or (time.perf_counter() - t0) < budget_s:
-        st, _ = ref.tebd_step_uniform(st, sched, scheme, pol)
+    while True:
+        one_update()
         n += 1
-        if time.perf_counter() - t0 > budget_s and n >= min_steps:
+        if n >= min_updates and time.perf_counter() - t0 >= budget_s:
+            break
+        if time.perf_counter() - t0 >= 4 * budget_s:
             break
     dt = time.perf_counter() - t0
-    return n / dt, n, dt
+    return (n / 3.0) / dt, n, dt
+
+
+def config_dict(cfg, ws):
+    """The `config` object both arms print (identical keys and values)."""
+    desc, d, chi, scheme, explicit, _ = cfg
+    eta, _ = widths(cfg)
+    return {"workload": desc, "d": d, "chi": chi, "eta": eta, "scheme": scheme, "cell_length": 2,
+            "explicit_error": explicit, "trotter_order": 2, "updates_per_step": 3,
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+            "l2": "flushed (256 MB write) between timed steps, outside the per-step event pair"}
 
 
 def run_reference(args, cfg):
-    ws, rank, _ = (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    ws, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     desc, d, chi, scheme, explicit, _ = cfg
-    # each "step" is a bounded sample: one full Trotter step of the oracle
-    rate, n, dt = cpu_reference_rate(cfg, budget_s=0.0, min_steps=max(1, args.steps), warmup=min(args.warmup, 1))
     cores = os.cpu_count()
+    # bounded sample: K steps' worth of updates on small cells; on large cells
+    # (north star: ~10 s per update on 16 cores) as many updates as fit in
+    # the budget, at least one -- the whole run stays within a few minutes
+    budget = float(os.environ.get("QT_REF_BUDGET_S", "60"))
+    warm = 1 if (args.warmup > 0 and chi <= 256) else 0
+    rate, n, dt = cpu_reference_rate(cfg, budget_s=budget if chi > 256 else 0.0,
+                                     min_updates=3 * max(1, args.steps) if chi <= 256 else 1, warmup_updates=warm)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
-        "steps": n, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 / rate, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / rate, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
-        "config": {"workload": desc, "d": d, "chi": chi, "scheme": scheme, "cell_length": 2,
-                   "explicit_error": explicit, "parallelism": "replicas"},
+        "config": config_dict(cfg, 1),
         "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} full Trotter steps of the NumPy/LAPACK oracle (OpenBLAS, {cores} threads)"},
+                         "sample": f"{n} bond updates ({n / 3:.2f} Trotter steps, {dt:.1f} s) of the NumPy/LAPACK "
+                                   f"oracle port in Trotter order on the same synthetic state and gates "
+                                   f"(OpenBLAS, {cores} threads); steps/s = updates/3 / time",
+                         "host": host_info()},
         "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def chain_config_dict(cc, ws):
+    """The `config` object both arms print for a finite chain."""
+    n = cc["n"]
+    upd = 2 * len(range(0, n - 1, 2)) + len(range(1, n - 1, 2))
+    return {"workload": cc["desc"], "n_sites": n, "d": cc["d"], "chi": cc["chi"], "scheme": cc["scheme"],
+            "explicit_error": cc["explicit"], "trotter_order": 2, "updates_per_step": upd,
+            "parallelism": f"sites sharded x{ws} (contiguous even-aligned blocks)",
+            "l2": "chain state (GBs) far larger than L2"}
 
 
 def run_chain(args, cc):
@@ -337,11 +390,7 @@ def run_chain(args, cc):
         "metric": METRIC, "value": 1e3 / ms_per_step, "unit": "steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
-        "config": {"workload": cc["desc"], "n_sites": n, "d": d, "chi": chi, "scheme": scheme,
-                   "explicit_error": explicit, "updates_per_step": upd_per_step,
-                   "parallelism": f"sites sharded x{ws} (contiguous even-aligned blocks); same-parity bonds on "
-                                  f"{max(1, nstreams)} concurrent streams per GPU",
-                   "l2": "chain state (GBs) far larger than L2"},
+        "config": chain_config_dict(cc, ws),
         "updates_per_s": upd_per_step * 1e3 / ms_per_step,
         "step_ms": [round(x, 3) for x in step_ms],
         "roofline": {"bound": "tensor", "achieved": f_step / (ms_per_step * 1e-3) / 1e12 * ws, "peak": dmma_peak * ws,
@@ -390,7 +439,7 @@ def run_chain_reference(args, cc):
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
             "steps": k, "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
-            "config": {"workload": cc["desc"], "n_sites": n, "d": d, "chi": chi},
+            "config": chain_config_dict(cc, int(os.environ.get("WORLD_SIZE", "1"))),
             "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": f"{k} central-bond updates (chi={chi}) of the NumPy/LAPACK oracle, step = "
                                        f"{upd} updates x mean update time (upper bound)"},
@@ -427,15 +476,18 @@ def gemm_traffic(config):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + sorted(CHAIN_CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS) + sorted(CHAIN_CONFIGS),
+                    help="default: north (N=1) / c5 sharded chain (N>1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--path", default="graph", choices=["graph", "value"],
                     help="graph: device-resident state, CUDA-graph step; value: C-ABI tebd_step (new handles)")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "north" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "c5"
     if args.config in CHAIN_CONFIGS:
         return run_chain(args, CHAIN_CONFIGS[args.config])
     cfg = CONFIGS[args.config]
@@ -554,34 +606,41 @@ def main():
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws) / args.steps
     d2h = sum(t.numel() * 8 for t in outs_pinned)
 
-    # ---------------- roofline of the dominant kernel (the DMMA GEMM)
-    achieved = gfl.value / (gmsl.value * 1e-3) / 1e12 if gmsl.value > 0 else 0.0
+    # ---------------- roofline: the whole step against the FP64 tensor pipe
+    # achieved = SURVEY.md §8(d) algorithmic flops of one Trotter step (3
+    # updates) / the device step time; the dominant DMMA GEMM kernel's own
+    # rate (event-bracketed launches inside the timed graph) is a sub-field
+    gemm_tf = gfl.value / (gmsl.value * 1e-3) / 1e12 if gmsl.value > 0 else 0.0
     eta, kk = widths(cfg)
     f_step = 3 * flops_per_update(d, chi, eta, kk, explicit, cbe=(scheme == "qr_cbe"))
+    step_tf = f_step / (ms_per_step * 1e-3) / 1e12
     roofline = {
-        "bound": "tensor", "achieved": achieved, "peak": dmma_peak, "unit": "TFLOP/s",
-        "frac": achieved / dmma_peak if dmma_peak else None, "traffic": gemm_traffic(args.config),
-        "kernel": "zgemm_kernel (mma.sync m8n8k4 f64 -> DMMA, TMA-staged): the hot-path contraction launches "
-                  f"(>= {prof_min_flops:.3g} flops each: theta build, X = theta Y0^H, Hastings, explicit-error "
-                  "products; the block-reflector products of the QR pair are not bracketed)",
-        "peak_source": "FP64 DMMA microbenchmark (csrc/probe.cu) measured in this run; MEASURED_PEAKS.json has no FP64",
-        "gemm_share_of_step": (gmsl.value / args.steps) / (sum(step_ms) / args.steps),
-        "gemm_launches_per_step": int(gll.value) / args.steps,
-        "step_achieved_tflops": f_step / (ms_per_step * 1e-3) / 1e12,
-        "step_frac": f_step / (ms_per_step * 1e-3) / 1e12 / dmma_peak,
+        "bound": "tensor", "achieved": step_tf, "peak": dmma_peak, "unit": "TFLOP/s",
+        "frac": step_tf / dmma_peak if dmma_peak else None, "traffic": gemm_traffic(args.config),
+        "scope": "whole Trotter step: SURVEY.md §8(d) algorithmic flops of 3 updates / device step time "
+                 "(QR panels, block reflectors, permutes and GEMMs all inside the denominator)",
         "flops_per_step": f_step,
+        "peak_source": "FP64 DMMA microbenchmark (csrc/probe.cu, mma.sync m8n8k4 f64 -> DMMA.8x8x4) measured in "
+                       "this run; MEASURED_PEAKS.json has no FP64 figure",
+        "traffic_note": "dram bytes per launch of the dominant GEMM shape from the committed ncu --set full "
+                        "capture (profiles/), null if none",
+        "dominant_kernel": {
+            "kernel": "zgemm_kernel (mma.sync m8n8k4 f64 -> DMMA, TMA-staged, mbarrier ring)",
+            "achieved": gemm_tf, "frac": gemm_tf / dmma_peak if dmma_peak else None,
+            "share_of_step": (gmsl.value / args.steps) / (sum(step_ms) / args.steps),
+            "launches_per_step": int(gll.value) / args.steps,
+            "bracketed": f"contraction launches >= {prof_min_flops:.3g} flops (theta build, X = theta Y0^H, "
+                         "Hastings, explicit-error products); the QR pair's block-reflector products are not "
+                         "bracketed"},
     }
 
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": ws, "steps": args.steps, "warmup": warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "complex128", "data": "synthetic",
-        "config": {"workload": desc, "d": d, "chi": chi, "scheme": scheme, "cell_length": 2,
-                   "explicit_error": explicit, "trotter_order": 2, "updates_per_step": 3,
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single",
-                   "path": ("device-resident state, one CUDA graph replay per step (qt_uniform_step)"
-                            if graph_path else "C-ABI qt_tebd_step_uniform, new handles per step"),
-                   "l2": "flushed (256 MB write) between timed steps, outside the per-step event pair"},
+        "config": config_dict(cfg, ws),
+        "path": ("device-resident state, one CUDA graph replay per step (qt_uniform_step)"
+                 if graph_path else "C-ABI qt_tebd_step_uniform, new handles per step"),
         "updates_per_s": 3 * value,
         "step_ms": [round(x, 3) for x in step_ms],
         "roofline": roofline,
@@ -592,17 +651,19 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, n, dt = cpu_reference_rate(cfg, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
-                                "sample": f"{n} Trotter steps ({dt:.1f} s) of the NumPy/LAPACK oracle on the same "
-                                          f"config, OpenBLAS threads = {os.cpu_count()}; LAPACK is likely faster "
-                                          "than the reference's Eigen, so speedups against it are conservative",
+                                "sample": f"{n} bond updates ({n / 3:.2f} Trotter steps, {dt:.1f} s) of the "
+                                          f"NumPy/LAPACK oracle port on the same config and state, OpenBLAS "
+                                          f"threads = {os.cpu_count()}; steps/s = updates/3 / time; LAPACK is "
+                                          "likely faster than the reference's Eigen, so speedups against it are "
+                                          "conservative",
                                 "host": host_info()}
-        # the reference's SVD-TEBD comparator (gates.cpp:312-322) on the same cell
-        # and truncation, timed beside it
-        cfg_svd = (cfg[0], cfg[1], cfg[2], "svd", cfg[4], cfg[5])
-        rate_s, n_s, dt_s = cpu_reference_rate(cfg_svd, budget_s=max(1.0, args.cpu_budget / 3))
-        line["cpu_baseline_svd"] = {"value": rate_s, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
-                                    "sample": f"{n_s} Trotter steps ({dt_s:.1f} s) of the oracle's SVD-TEBD update "
-                                              "(zgesdd of theta) on the same state and gate schedule"}
+        if chi <= 256:
+            # the reference's SVD-TEBD comparator (gates.cpp:312-322) on the
+            # same cell and truncation, timed beside it
+            rate_s, n_s, dt_s = cpu_reference_rate(cfg, budget_s=max(1.0, args.cpu_budget / 3), scheme="svd")
+            line["cpu_baseline_svd"] = {"value": rate_s, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+                                        "sample": f"{n_s} updates ({dt_s:.1f} s) of the oracle's SVD-TEBD update "
+                                                  "(zgesdd of theta) on the same state and gate schedule"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if graph_path:

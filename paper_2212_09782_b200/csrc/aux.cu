@@ -101,6 +101,7 @@ void* Engine::raw(int slot, size_t bytes) {
       QT_CUDA(cudaFree(slot_ptr[slot]));
       slot_ptr[slot] = nullptr;
       slot_bytes[slot] = 0;
+      ++arena_gen;
     }
     // round up to limit regrowth churn
     size_t want = bytes + bytes / 8;

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/qrtebd_c.h).  Thin: validates shapes with the
 // reference's error taxonomy, allocates output handles, calls the engine.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -580,7 +581,8 @@ qt_status qt_tebd_step_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* con
     };
     std::vector<Pending> pend;
     std::vector<qt_report> reps;
-    double* rep_dev = ctx->eng.dbuf(qt::S_REPORTS, 4 * (n_layers * (L / 2 + 1) + 1));
+    // 8 report doubles per update: the scalars and the SC_TMP3 finiteness flag
+    double* rep_dev = ctx->eng.dbuf(qt::S_REPORTS, 8 * (n_layers * (L / 2 + 1) + 1));
     for (uint64_t l = 0; l < n_layers; ++l) {
       const qt_tensor* u = gates[l];
       require_gate(u, d);
@@ -593,7 +595,7 @@ qt_status qt_tebd_step_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* con
           const long long eta = qt::qr_eta(pol, D);
           QrOut o = launch_qr(ctx, D, cur_b[m], cur_s[m], cur_s[n], u, pol, eta, false);
           // stash the report scalars of this update (no host sync inside the step)
-          QT_CUDA(cudaMemcpyAsync(rep_dev + 4 * pend.size(), ctx->eng.dscal, 4 * sizeof(double),
+          QT_CUDA(cudaMemcpyAsync(rep_dev + 8 * pend.size(), ctx->eng.dscal, 8 * sizeof(double),
                                   cudaMemcpyDeviceToDevice, ctx->eng.stream));
           pend.push_back({n, static_cast<uint64_t>(D.chi_n), static_cast<uint64_t>(eta)});
           nbm = o.b_m;
@@ -637,16 +639,20 @@ qt_status qt_tebd_step_uniform(qt_ctx* ctx, uint64_t cell_length, qt_tensor* con
       }
     }
     if (scheme == QT_SCHEME_QR) {
-      std::vector<double> h(4 * pend.size() + 4);
+      std::vector<double> h(8 * pend.size() + 8);
       if (!pend.empty())
-        QT_CUDA(cudaMemcpyAsync(h.data(), rep_dev, 4 * pend.size() * sizeof(double), cudaMemcpyDeviceToHost,
+        QT_CUDA(cudaMemcpyAsync(h.data(), rep_dev, 8 * pend.size() * sizeof(double), cudaMemcpyDeviceToHost,
                                 ctx->eng.stream));
       QT_CUDA(cudaStreamSynchronize(ctx->eng.stream));
       for (size_t i = 0; i < pend.size(); ++i) {
         qt::HostReport hr;
-        hr.theta2 = h[4 * i + qt::SC_THETA2];
-        hr.kept2 = h[4 * i + qt::SC_L2];
-        hr.resid = h[4 * i + qt::SC_RESID];
+        hr.theta2 = h[8 * i + qt::SC_THETA2];
+        hr.kept2 = h[8 * i + qt::SC_L2];
+        hr.resid = h[8 * i + qt::SC_RESID];
+        int fl = 0;
+        std::memcpy(&fl, &h[8 * i + qt::SC_TMP3], sizeof(int));
+        // require_finite_matrix, proj/src/linalg.cpp:17-21
+        if (fl != 0) throw qt::Error(qt::Err::input, "qr_reduced: non-finite entries");
         double eps = 0, disc = 0;
         report_from(hr, pol, &eps, &disc);
         qt_report r;
@@ -817,12 +823,31 @@ qt_status qt_eigh(qt_ctx* ctx, const qt_tensor* h, double* w_host, qt_tensor** v
     if (h->shape[0] != h->shape[1]) throw qt::Error(qt::Err::shape, "eigh: matrix not square");
     qt::Engine& e = ctx->eng;
     const long long n = h->shape[0];
+    // require_finite_matrix + the hermiticity check of proj/src/linalg.cpp:80-86:
+    // InputError when ||h - h^H||_F > 1e-10 max(||h||_F, 1e-300)
+    {
+      int* flag = reinterpret_cast<int*>(e.dscal + qt::SC_TMP3);
+      QT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), e.stream));
+      qt::check_finite(e, h->data, n * n, flag);
+      qt::hermitian_defect(e, h->data, n, e.dscal + qt::SC_TMP0);
+      QT_CUDA(cudaMemcpyAsync(e.hscal, e.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+      QT_CUDA(cudaStreamSynchronize(e.stream));
+      int hflag = 0;
+      std::memcpy(&hflag, &e.hscal[qt::SC_TMP3], sizeof(int));
+      if (hflag) throw qt::Error(qt::Err::input, "eigh: non-finite entries");
+      const double defect = std::sqrt(e.hscal[qt::SC_TMP0]), nrm = std::sqrt(e.hscal[qt::SC_TMP1]);
+      if (defect > 1e-10 * std::max(nrm, 1e-300))
+        throw qt::Error(qt::Err::input, "eigh: matrix not hermitian within tolerance");
+    }
     qt_tensor* v = new_tensor(ctx, {static_cast<uint64_t>(n), static_cast<uint64_t>(n)});
     try {
       double* w = e.dbuf(qt::S_EIG_W, n + 8);
-      qt::eigh_device(e, h->data, n, w, v->data);
+      const int* esw = qt::eigh_device(e, h->data, n, w, v->data);
+      int status = 1;
       QT_CUDA(cudaMemcpyAsync(w_host, w, n * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+      if (esw) QT_CUDA(cudaMemcpyAsync(&status, esw, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
       QT_CUDA(cudaStreamSynchronize(e.stream));
+      qt::require_eigh_converged(status);
     } catch (...) {
       free_tensor(v);
       throw;

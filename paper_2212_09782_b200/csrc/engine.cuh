@@ -98,6 +98,9 @@ struct Engine {
   // engine (-1: the library default); contexts that run side by side with
   // other contexts (sharded chains) raise it (qt_ctx_set_qr_pair_min_rows)
   long long qr_pair_min_rows = -1;
+  // bumped whenever raw() frees and reallocates a slot: captured CUDA graphs
+  // hold raw slot pointers and must be recaptured after a regrowth
+  unsigned long long arena_gen = 0;
 
   void init(int dev, cudaStream_t st);
   void destroy();

@@ -91,7 +91,12 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
 
 // eigh of a Hermitian n x n matrix on the device (proj/src/linalg.cpp:79-101):
 // eigenvalues descending into w (device), eigenvectors as columns of v (device, ld n)
-void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v);
+// Returns a device pointer to the solver status word: > 0 sweeps to
+// convergence, < 0 no convergence within the sweep cap (require_eigh_converged).
+const int* eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v);
+void require_eigh_converged(int status);
+// out2[0] = ||h - h^H||_F^2, out2[1] = ||h||_F^2 (device, deterministic)
+void hermitian_defect(Engine& e, const double2* h, long long n, double* out2);
 // singular values of an arbitrary p x q matrix, descending; returns a device
 // pointer (engine slot S_EIG_W) to min(p,q) values
 double* singular_values_device(Engine& e, const double2* m, long long p, long long q);

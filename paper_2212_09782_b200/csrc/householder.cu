@@ -283,12 +283,11 @@ void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs, cudaStream_t 
     return RPW <= 5 ? mx : size_t(0);
   }();
   constexpr size_t smem_attr = pre_smem > panel_cluster_smem(RPW) ? pre_smem : panel_cluster_smem(RPW);
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_attr)));
-    attr = true;
-  }
+  });
   if (a.pre && RPW > 5) throw Error(Err::internal, "fused panel look-ahead needs <= 5 rows per warp");
   const size_t smem = a.pre ? std::max(panel_cluster_smem(RPW), panel_pre_smem<RPW>(static_cast<int>(cs)))
                             : panel_cluster_smem(RPW);
@@ -309,13 +308,14 @@ void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs, cudaStream_t 
 }
 
 bool launch_panel_cluster(Engine& e, const PanelArgs& base, long long mp, cudaStream_t st) {
-  static int max_cs = -1;
-  if (max_cs < 0) {
+  // probed once, thread-safe (magic static): concurrent first calls from the
+  // chain's bond threads must agree on the path
+  static const int max_cs = [] {
     auto kern = panel_cluster_kernel<CL_MAX_RPW>;
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const size_t smem_max = panel_cluster_smem(CL_MAX_RPW);
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_max)));
-    max_cs = 0;
+    int found = 0;
     for (int cs : {16, 8}) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs);
@@ -330,12 +330,13 @@ bool launch_panel_cluster(Engine& e, const PanelArgs& base, long long mp, cudaSt
       cfg.numAttrs = 1;
       int n = 0;
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1) {
-        max_cs = cs;
+        found = cs;
         break;
       }
       cudaGetLastError();
     }
-  }
+    return found;
+  }();
   if (max_cs == 0) return false;
   // as many CTAs as the cluster allows (short per-warp row loops), >= 32 rows
   // each so CTA 0 owns the whole diagonal block
@@ -380,11 +381,12 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp, cudaStream_t s
   PanelArgs a = base;
   a.rpc = static_cast<int>(rpc);
   const size_t smem = (size_t(rpc) * NB + PANEL_WARPS * NB + NB * NB + 2 * NB) * sizeof(double2);
-  static size_t attr = 0;
-  if (smem > attr) {
-    QT_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = smem;
-  }
+  static std::once_flag attr_once;  // the largest panel (rpc <= 1024) fits 227 KB
+  std::call_once(attr_once, [] {
+    QT_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>((size_t(1024) * NB + PANEL_WARPS * NB + NB * NB + 2 * NB) *
+                                                  sizeof(double2))));
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(G));
   cfg.blockDim = dim3(PANEL_THREADS);
@@ -529,12 +531,11 @@ constexpr size_t apply_cols_smem() {
 
 void apply_cols(const double2* Vp, long long ldv, const double2* Tp, int nbp, double2* C, long long ldc, long long mp,
                 long long nc, const double2* xa, long long lda, double2* yh, long long ldy, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
     QT_CUDA(cudaFuncSetAttribute(apply_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(apply_cols_smem())));
-    attr = true;
-  }
+  });
   apply_cols_kernel<<<static_cast<unsigned>(ceil_div(nc, AC_CB)), AC_THREADS, apply_cols_smem(), st>>>(
       Vp, ldv, Tp, nbp, C, ldc, mp, nc, xa, lda, yh, ldy);
   QT_LAUNCHED();

@@ -23,6 +23,8 @@
 // at most 30 sweeps.  Every reduction has a fixed order: results are bitwise
 // reproducible run to run.
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 
 #include "gate.cuh"
 
@@ -395,6 +397,7 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   if (R1 == 1) publish(0);
   jgrid_sync(a.bar, G, epoch);
   int sw = 0, rd = 0;
+  bool conv = false;
   for (;;) {
     long long t0 = stamp ? clock64() : 0;
     bool done = false;
@@ -477,6 +480,7 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     if (stamp) pb += clock64() - t1;
     if (doA && nr == R1 - 1) publish(ns);
     if (!doA) {
+      conv = done;
       sw = ns;
       break;
     }
@@ -486,7 +490,8 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     sw = ns;
     rd = nr;
   }
-  if (cta == 0 && tid == 0) *a.sweeps_out = sw;
+  // > 0: sweeps to convergence; < 0: stopped at MAX_SWEEPS without converging
+  if (cta == 0 && tid == 0) *a.sweeps_out = conv ? max(sw, 1) : -max(sw, 1);
   if (stamp) {
     a.prof[0] = pa;
     a.prof[1] = pw;
@@ -581,8 +586,8 @@ __global__ void sqrt_clip_kernel(const double* __restrict__ w, int n, double* s)
 
 }  // namespace
 
-void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v) {
-  if (n <= 0) return;
+const int* eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v) {
+  if (n <= 0) return nullptr;
   // 16-wide blocks (32x32 subproblems) below n = 512, 32-wide above: the
   // subproblem sweep is the critical path for small n, the tile updates for large n
   static const int jb_env = std::getenv("QT_JACOBI_JB") ? std::atoi(std::getenv("QT_JACOBI_JB")) : 0;
@@ -631,11 +636,10 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   a.fro2 = fro;
   const size_t jsmem = 3 * JX * (JX + 1) * sizeof(double2);
   auto kern = JB == 16 ? jacobi_kernel<16> : jacobi_kernel<32>;
-  static bool jattr[2] = {false, false};
-  if (!jattr[JB == 32]) {
+  static std::once_flag jattr[2];
+  std::call_once(jattr[JB == 32], [&] {
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(jsmem)));
-    jattr[JB == 32] = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(JT);
@@ -676,18 +680,131 @@ void eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v
   while (P < N) P <<= 1;
   const size_t smem = static_cast<size_t>(P) * (sizeof(double) + sizeof(int));
   if (smem > 200 * 1024) throw Error(Err::capacity, "eigh: matrix too large for the device sort");
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    QT_CUDA(cudaFuncSetAttribute(jacobi_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    attr = smem;
-  }
+  static std::once_flag attr_once;  // set once to the cap checked above (no lost updates across threads)
+  std::call_once(attr_once, [] {
+    QT_CUDA(cudaFuncSetAttribute(jacobi_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  });
   int* idx = reinterpret_cast<int*>(cta_max + 2 * grid + 8 + ngt / 2 + 1);
   jacobi_sort_kernel<<<1, 1024, smem, e.stream>>>(G, static_cast<int>(n), N, fro, w, idx);
   QT_LAUNCHED();
   const long long nn = static_cast<long long>(n) * n;
   jacobi_gather_kernel<<<static_cast<int>(std::min<long long>(ceil_div(nn, 256), 4 * e.num_sms)), 256, 0, e.stream>>>(
       V, static_cast<int>(n), N, idx, v);
+  QT_LAUNCHED();
+  return sweeps;
+}
+
+void require_eigh_converged(int status) {
+  // Eigen's SelfAdjointEigenSolver info() != Success -> NumericError (proj/src/linalg.cpp:88-90)
+  if (status <= 0) throw Error(Err::numeric, "eigh: factorization did not converge");
+}
+
+namespace {
+// per-row partial sums of |h_ij - conj(h_ji)|^2 and |h_ij|^2 (one CTA per row,
+// fixed-order tree: deterministic)
+__global__ void herm_defect_rows_kernel(const double2* __restrict__ h, int n, double* rows) {
+  __shared__ double sd[256], sn[256];
+  const int i = blockIdx.x;
+  double acc_d = 0.0, acc_n = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double2 a = h[static_cast<long long>(i) * n + j], b = h[static_cast<long long>(j) * n + i];
+    const double dr = a.x - b.x, di = a.y + b.y;
+    acc_d += dr * dr + di * di;
+    acc_n += a.x * a.x + a.y * a.y;
+  }
+  sd[threadIdx.x] = acc_d;
+  sn[threadIdx.x] = acc_n;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      sd[threadIdx.x] += sd[threadIdx.x + st];
+      sn[threadIdx.x] += sn[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    rows[2 * i] = sd[0];
+    rows[2 * i + 1] = sn[0];
+  }
+}
+
+__global__ void herm_defect_sum_kernel(const double* __restrict__ rows, int n, double* out2) {
+  __shared__ double sd[256], sn[256];
+  double acc_d = 0.0, acc_n = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    acc_d += rows[2 * i];
+    acc_n += rows[2 * i + 1];
+  }
+  sd[threadIdx.x] = acc_d;
+  sn[threadIdx.x] = acc_n;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      sd[threadIdx.x] += sd[threadIdx.x + st];
+      sn[threadIdx.x] += sn[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out2[0] = sd[0];
+    out2[1] = sn[0];
+  }
+}
+
+// s_k^2 = || B[:, k] ||^2 over the rows of B (rows x k, ld k): one warp per
+// column, fixed lane order -> deterministic
+__global__ void colnorm2_kernel(const double2* __restrict__ b, long long rows, int k, double* s2) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= k) return;
+  double acc = 0.0;
+  for (long long r = lane; r < rows; r += 32) {
+    const double2 v = b[r * k + warp];
+    acc = fma(v.x, v.x, fma(v.y, v.y, acc));
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) s2[warp] = acc;
+}
+
+// s = sqrt(s2) sorted descending (ties: lower index first), one CTA bitonic
+__global__ void sqrt_sort_desc_kernel(const double* __restrict__ s2, int k, double* s) {
+  extern __shared__ unsigned char ssm[];
+  int P = 1;
+  while (P < k) P <<= 1;
+  double* key = reinterpret_cast<double*>(ssm);
+  int* idx = reinterpret_cast<int*>(key + P);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    key[i] = i < k ? sqrt(fmax(s2[i], 0.0)) : -1.0;
+    idx[i] = i;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          const bool i_first = (key[i] > key[j]) || (key[i] == key[j] && idx[i] < idx[j]);
+          if (desc != i_first) {
+            const double tk = key[i];
+            key[i] = key[j];
+            key[j] = tk;
+            const int ti = idx[i];
+            idx[i] = idx[j];
+            idx[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s[i] = key[i];
+}
+}  // namespace
+
+void hermitian_defect(Engine& e, const double2* h, long long n, double* out2) {
+  double* rows = e.dbuf(S_QR_PART, 2 * n + 8);
+  herm_defect_rows_kernel<<<static_cast<int>(n), 256, 0, e.stream>>>(h, static_cast<int>(n), rows);
+  QT_LAUNCHED();
+  herm_defect_sum_kernel<<<1, 256, 0, e.stream>>>(rows, static_cast<int>(n), out2);
   QT_LAUNCHED();
 }
 
@@ -760,11 +877,11 @@ bool diagonal_singular_values(Engine& e, const double2* m, long long p, long lon
   int P = 1;
   while (P < k) P <<= 1;
   const size_t smem = static_cast<size_t>(P) * (sizeof(double) + sizeof(int));
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    QT_CUDA(cudaFuncSetAttribute(diag_sv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = smem;
-  }
+  if (smem > 200 * 1024) return false;
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    QT_CUDA(cudaFuncSetAttribute(diag_sv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  });
   diag_sv_kernel<<<1, 1024, smem, e.stream>>>(m, q, static_cast<int>(k), s);
   QT_LAUNCHED();
   return true;
@@ -805,7 +922,38 @@ double* singular_values_device(Engine& e, const double2* m, long long p, long lo
   double* w = e.dbuf(S_EIG_W, g + 8);
   double2* v = e.cbuf(S_MISC2, g * g);
   eigh_device(e, gm, g, w, v);
-  sqrt_clip_kernel<<<1, 256, 0, e.stream>>>(w, static_cast<int>(k), w);
+  // Rayleigh-Ritz refinement: the Gram eigenvalues carry an absolute error
+  // ~u s_0^2, i.e. ~sqrt(u) s_0 in the small singular values; the Gram
+  // eigenvectors are accurate to ~u in angle, so the column norms of
+  // B = op(m) v (tall: m v; wide: m^H v) give every s_k to ~u s_0 absolute
+  // (|ds_k| <= 1e-10 s_0), then sort descending
+  const long long rows = wide ? q : p;
+  double2* bm = e.cbuf(S_QR_W, rows * g);
+  GemmDesc r;
+  r.M = rows;
+  r.N = g;
+  r.K = g;
+  r.opA = wide ? Op::H : Op::N;
+  r.A = m;
+  r.lda = q;
+  r.opB = Op::N;
+  r.B = v;
+  r.ldb = g;
+  r.C = bm;
+  r.ldc = g;
+  zgemm(r, e.gemm_scratch(), e.stream);
+  double* s2 = e.dbuf(S_MISC, g + 8);
+  colnorm2_kernel<<<static_cast<int>(ceil_div(g * 32, 256)), 256, 0, e.stream>>>(bm, rows, static_cast<int>(g), s2);
+  QT_LAUNCHED();
+  int P = 1;
+  while (P < k) P <<= 1;
+  const size_t smem = static_cast<size_t>(P) * (sizeof(double) + sizeof(int));
+  if (smem > 200 * 1024) throw Error(Err::capacity, "schmidt_values: matrix too large for the device sort");
+  static std::once_flag once;
+  std::call_once(once, [] {
+    QT_CUDA(cudaFuncSetAttribute(sqrt_sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  });
+  sqrt_sort_desc_kernel<<<1, 1024, smem, e.stream>>>(s2, static_cast<int>(k), w);
   QT_LAUNCHED();
   return w;
 }

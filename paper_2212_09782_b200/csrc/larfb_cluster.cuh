@@ -229,13 +229,12 @@ constexpr size_t larfb_cluster_smem(int rpc, int cs, int cw) {
 template <int CW>
 void larfb_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv, const double2* T, double2* A,
                   long long lda, long long mp, long long ncols, int nbp, long long rpc, bool use_th, long long* dbg) {
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
     QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<CW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(larfb_cluster_smem(LB_MAX_RPC, 16, 32))));
-    attr = true;
-  }
+  });
   QT_CUDA(cudaLaunchKernelEx(&cfg, larfb_cluster_kernel<CW>, V, ldv, T, A, lda, static_cast<int>(mp),
                              static_cast<int>(ncols), nbp, static_cast<int>(rpc), use_th ? 1 : 0, dbg));
 }
@@ -244,12 +243,11 @@ void larfb_launch(cudaLaunchConfig_t& cfg, const double2* V, long long ldv, cons
 // reflectors; returns false when the panel is too tall for one cluster.
 // largest cluster the block-reflector kernel can run with (16, 8 or 0)
 int larfb_max_cs() {
-  static int max_cs = -1;
-  if (max_cs < 0) {
+  static const int max_cs = [] {  // probed once, thread-safe (magic static)
     QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     QT_CUDA(cudaFuncSetAttribute(larfb_cluster_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(larfb_cluster_smem(LB_MAX_RPC, 16, 32))));
-    max_cs = 0;
+    int found = 0;
     for (int cs : {16, 8}) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs, 1);
@@ -264,12 +262,13 @@ int larfb_max_cs() {
       cfg.numAttrs = 1;
       int n = 0;
       if (cudaOccupancyMaxActiveClusters(&n, larfb_cluster_kernel<32>, &cfg) == cudaSuccess && n >= 1) {
-        max_cs = cs;
+        found = cs;
         break;
       }
       cudaGetLastError();
     }
-  }
+    return found;
+  }();
   return max_cs;
 }
 

@@ -34,6 +34,7 @@ struct UniformDev {
     cudaGraphExec_t exec = nullptr;
     std::vector<GemmProfRec> prof;
     unsigned long long kernels = 0;  // kernel nodes in the graph
+    unsigned long long arena_gen = 0;  // workspace generation the graph's pointers belong to
   };
   std::map<std::string, GraphEntry> graphs;
   std::map<std::string, int> seen;
@@ -45,6 +46,12 @@ struct UniformDev {
   std::vector<Engine*> aux;
   std::vector<cudaEvent_t> ev;
 
+  // sum of the workspace generations of every engine a step touches
+  unsigned long long arena_gen() const {
+    unsigned long long g = e->arena_gen;
+    for (const Engine* a : aux) g += a->arena_gen;
+    return g;
+  }
   long long site_elems(int m) const { return d * chi[m] * chi[(m + 1) % L]; }
   long long bond_elems(int m) const { return chi[m] * chi[m]; }
 };
@@ -278,6 +285,19 @@ std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<
     for (const Upd& u : ups) put(&u.u, sizeof(u.u));
     put(&pol, sizeof(pol));
     auto it = s->graphs.find(key);
+    if (it != s->graphs.end() && it->second.arena_gen != s->arena_gen()) {
+      // a workspace slot was reallocated since the capture (another call on
+      // this context grew it): the graph's pointers are stale -- run this
+      // step eagerly and recapture on the next one
+      cudaGraphExecDestroy(it->second.exec);
+      for (auto& r : it->second.prof) {
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+      }
+      s->graphs.erase(it);
+      it = s->graphs.end();
+      s->seen[key] = 0;
+    }
     if (it == s->graphs.end() && s->seen[key] >= 1) {
       // buffers are sized by an earlier eager step with the same key: capture
       cudaGraph_t g = nullptr;
@@ -293,6 +313,7 @@ std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<
       }
       QT_CUDA(cudaStreamEndCapture(e.stream, &g));
       UniformDev::GraphEntry ge;
+      ge.arena_gen = s->arena_gen();
       QT_CUDA(cudaGraphInstantiate(&ge.exec, g, 0));
       QT_CUDA(cudaGraphDestroy(g));
       ge.prof = gemm_profile_take_captured();

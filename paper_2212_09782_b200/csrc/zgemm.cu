@@ -447,11 +447,10 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
   using C_ = Cfg<OPA, OPB, WGM, WGN, WTM, WTN, BK, STAGES>;
   constexpr int BM = C_::BM, BN = C_::BN;
   auto kern = zgemm_kernel<OPA, OPB, WGM, WGN, WTM, WTN, BK, STAGES, MODE>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C_::SMEM)));
-    attr_set = true;
-  }
+  });
   const int a_bz = (d.batch > 1 && d.strideA != 0) ? 1 : 0;
   const int b_bz = (d.batch > 1 && d.strideB != 0) ? 1 : 0;
   const int ba = a_bz ? d.batch : 1, bb = b_bz ? d.batch : 1;

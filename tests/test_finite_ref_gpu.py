@@ -100,8 +100,7 @@ def test_finite_step_matches_oracle(ctx, scheme, chi_max, n, d):
             so = ref.schmidt_values_finite(orc, b)
             sd = spectra[b]
             assert len(sd) == len(so)
-            big = so >= 1e-6 * so[0]  # the Gram route resolves values above ~1e-8 s0
-            assert np.max(np.abs(sd[big] - so[big])) <= 1e-10 * so[0]
+            assert np.max(np.abs(sd - so)) <= 1e-10 * so[0]  # every value (Appendix B (ii))
             assert abs(ref.entropy_from_schmidt(sd) - ref.entropy_from_schmidt(so)) < 1e-10
 
 

@@ -135,7 +135,8 @@ def test_pair_concurrent_cell_L4_matches_oracle(ctx, chi):
         assert abs(q.expectation_local(snap, z, m, ctx) - ref.expectation_local(st, z, m)) < 1e-10
         sd = q.schmidt_values(snap, m, ctx)
         so = ref.schmidt_values(st, m)
-        assert np.max(np.abs(sd[: len(so)] - so)[so >= 1e-6 * so[0]]) <= 1e-10 * so[0]
+        # every Schmidt value, no filter
+        assert sd.shape == so.shape and np.max(np.abs(sd - so)) <= 1e-10 * so[0]
 
 
 def test_pair_and_sequential_paths_agree_per_context_knob():

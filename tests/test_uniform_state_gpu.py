@@ -134,3 +134,48 @@ def test_check_isometric_matches_oracle(ctx, L, chi):
     st2 = ref.UniformMPS(d, [t.numpy() for t in st.site_tensors], [b.numpy() for b in st.bond_matrices])
     ok2, mx2, _ = ref.check_isometric_uniform(st2, 1e-6)
     assert rep2.passed == ok2 and abs(rep2.max_defect() - mx2) <= 1e-12
+
+
+def test_graph_recaptured_after_workspace_regrowth():
+    """Cached step graphs hold raw workspace pointers: a call on the same
+    context that grows a workspace slot (here a larger-chi update) must not
+    leave the next replay writing freed memory -- the graph is dropped and
+    recaptured, and the trajectory stays bitwise equal to an eager one."""
+    from paper_2212_09782_b200._capi import Context
+    d, chi, big = 3, 16, 48
+    sched = model.trotter_schedule(model.bond_hamiltonian(d, 2.0), 0.05, 2)
+    pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0)
+    pol_big = q.TruncationPolicy(chi_max=big, delta_chi_abs=0, delta_chi_rel=0.0)
+    with Context(0) as c1, Context(0) as c2:
+        gates1 = [(p, c1.tensor(g)) for p, g in sched]
+        gates2 = [(p, c2.tensor(g)) for p, g in sched]
+        dev_g = q.DeviceUniformMPS(random_state(c1, d, chi, 5), c1)
+        dev_e = q.DeviceUniformMPS(random_state(c2, d, chi, 5), c2)
+        st_big = random_state(c1, d, big, 6)
+        for k in range(8):
+            dev_g.step(gates1, "qr", pol, use_graph=True)
+            dev_e.step(gates2, "qr", pol, use_graph=False)
+            if k in (3, 5):  # grow the context's workspace between replays
+                q.tebd_step(st_big, gates1, "qr", pol_big, c1)
+                q.bond_energy(st_big.bond_matrices[0].numpy(), st_big.site_tensors[0].numpy(),
+                              st_big.site_tensors[1].numpy(), model.bond_hamiltonian(d, 2.0), c1)
+            for m in range(2):
+                assert np.array_equal(dev_g.view("site", m).numpy(), dev_e.view("site", m).numpy())
+                assert np.array_equal(dev_g.view("bond", m).numpy(), dev_e.view("bond", m).numpy())
+        dev_g.close()
+        dev_e.close()
+
+
+def test_tebd_step_rejects_non_finite_state(ctx):
+    """require_finite_matrix (proj/src/linalg.cpp:17-21) through the uniform
+    step: a NaN in the state raises InputError, as apply_gate_qr does."""
+    from paper_2212_09782_b200._capi import InputError
+    d, chi = 3, 8
+    rng = np.random.default_rng(3)
+    sites = [ref.random_right_isometry(rng, d, chi, chi) for _ in range(2)]
+    bonds = [np.eye(chi, dtype=complex) / np.sqrt(chi) for _ in range(2)]
+    sites[1][1, 2, 3] = np.nan
+    st = q.UniformMPS.from_numpy(ctx, d, sites, bonds)
+    sched = [(p, ctx.tensor(g)) for p, g in model.trotter_schedule(model.bond_hamiltonian(d, 2.0), 0.05, 2)]
+    with pytest.raises(InputError):
+        q.tebd_step(st, sched, "qr", q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0), ctx)
