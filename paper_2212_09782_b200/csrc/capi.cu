@@ -842,12 +842,12 @@ qt_status qt_eigh(qt_ctx* ctx, const qt_tensor* h, double* w_host, qt_tensor** v
     qt_tensor* v = new_tensor(ctx, {static_cast<uint64_t>(n), static_cast<uint64_t>(n)});
     try {
       double* w = e.dbuf(qt::S_EIG_W, n + 8);
-      const int* esw = qt::eigh_device(e, h->data, n, w, v->data);
-      int status = 1;
+      const qt::EighStatus* esw = qt::eigh_device(e, h->data, n, w, v->data);
+      qt::EighStatus status{1, 0, 0.0, 0.0};
       QT_CUDA(cudaMemcpyAsync(w_host, w, n * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
-      if (esw) QT_CUDA(cudaMemcpyAsync(&status, esw, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
+      if (esw) QT_CUDA(cudaMemcpyAsync(&status, esw, sizeof(status), cudaMemcpyDeviceToHost, e.stream));
       QT_CUDA(cudaStreamSynchronize(e.stream));
-      qt::require_eigh_converged(status);
+      qt::require_eigh_converged(status, n);
     } catch (...) {
       free_tensor(v);
       throw;

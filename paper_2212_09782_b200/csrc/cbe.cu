@@ -130,15 +130,15 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
   gemm2(e, Op::N, Op::H, eta, eta, eta, Rp, eta, Rp, eta, gm, eta);
   double* w = e.dbuf(S_EIG_W, eta + 8);
   double2* V = e.cbuf(S_MISC2, eta * eta);
-  const int* esw = eigh_device(e, gm, eta, w, V);
+  const EighStatus* esw = eigh_device(e, gm, eta, w, V);
 
   std::vector<double> wh(static_cast<size_t>(eta));
-  int eig_status = 1;
+  EighStatus eig_status{1, 0, 0.0, 0.0};
   QT_CUDA(cudaMemcpyAsync(wh.data(), w, eta * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
   QT_CUDA(cudaMemcpyAsync(e.hscal, e.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, e.stream));
-  if (esw) QT_CUDA(cudaMemcpyAsync(&eig_status, esw, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
+  if (esw) QT_CUDA(cudaMemcpyAsync(&eig_status, esw, sizeof(EighStatus), cudaMemcpyDeviceToHost, e.stream));
   QT_CUDA(cudaStreamSynchronize(e.stream));
-  require_eigh_converged(eig_status);
+  require_eigh_converged(eig_status, eta);
   int fl = 0;
   std::memcpy(&fl, &e.hscal[SC_TMP3], sizeof(int));
   if (fl) throw Error(Err::input, "qr_reduced: non-finite entries");

@@ -91,10 +91,17 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
 
 // eigh of a Hermitian n x n matrix on the device (proj/src/linalg.cpp:79-101):
 // eigenvalues descending into w (device), eigenvectors as columns of v (device, ld n)
-// Returns a device pointer to the solver status word: > 0 sweeps to
-// convergence, < 0 no convergence within the sweep cap (require_eigh_converged).
-const int* eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v);
-void require_eigh_converged(int status);
+// Returns a device pointer to the solver status (sweeps > 0: a full sweep
+// rotated nothing; < 0: stopped at the sweep cap -- then the off-diagonal mass
+// left decides, require_eigh_converged).
+struct EighStatus {
+  int sweeps;
+  int pad;
+  double offdiag2;  // ||offdiag(G_final)||_F^2 (scaled frame)
+  double fro2;      // ||G||_F^2 (scaled frame)
+};
+const EighStatus* eigh_device(Engine& e, const double2* h, long long n, double* w, double2* v);
+void require_eigh_converged(const EighStatus& st, long long n);
 // out2[0] = ||h - h^H||_F^2, out2[1] = ||h||_F^2 (device, deterministic)
 void hermitian_defect(Engine& e, const double2* h, long long n, double* out2);
 // singular values of an arbitrary p x q matrix, descending; returns a device
