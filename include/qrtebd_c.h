@@ -247,6 +247,14 @@ qt_status qt_finite_move_center(qt_finite* f, uint64_t new_center);
  * moves the center to m+1, QR_CBE keeps the center and renormalizes b_m. */
 qt_status qt_finite_step(qt_finite* f, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
                          qt_scheme scheme, const qt_policy* policy, qt_bond_report* reports, uint64_t* n_reports);
+/* The same with an observer (FiniteGateObserver, proj/include/qrtebd/gates.hpp:
+ * 120-123, :149-152) called after every gate with that gate's report; the
+ * state (qt_finite_view) is consistent and synchronized inside the call.  A
+ * nonzero return aborts the step with QT_ERR_INTERNAL. */
+typedef int (*qt_gate_observer)(void* user, const qt_bond_report* report);
+qt_status qt_finite_step_observed(qt_finite* f, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
+                                  qt_scheme scheme, const qt_policy* policy, qt_bond_report* reports,
+                                  uint64_t* n_reports, qt_gate_observer observer, void* user);
 /* expectation_local(FiniteMPS) (mps.cpp:188-196) on every site and
  * schmidt_values(FiniteMPS) (mps.cpp:203-207) of every bond 0..n, from one
  * gauge sweep over a copy of the state.  z_out: 2n doubles or NULL (op NULL

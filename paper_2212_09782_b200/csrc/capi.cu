@@ -1148,6 +1148,12 @@ qt_status qt_finite_move_center(qt_finite* f, uint64_t new_center) {
 
 qt_status qt_finite_step(qt_finite* f, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
                          qt_scheme scheme, const qt_policy* policy, qt_bond_report* reports, uint64_t* n_reports) {
+  return qt_finite_step_observed(f, n_layers, parity, gates, scheme, policy, reports, n_reports, nullptr, nullptr);
+}
+
+qt_status qt_finite_step_observed(qt_finite* f, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
+                                  qt_scheme scheme, const qt_policy* policy, qt_bond_report* reports,
+                                  uint64_t* n_reports, qt_gate_observer observer, void* user) {
   return guard([&] {
     require(f && (n_layers == 0 || (parity && gates)), qt::Err::input, "qt_finite_step: null argument");
     if (scheme != QT_SCHEME_QR && scheme != QT_SCHEME_QR_CBE)
@@ -1221,6 +1227,7 @@ qt_status qt_finite_step(qt_finite* f, uint64_t n_layers, const int32_t* parity,
           f->sites[m + 1] = bn;
           f->center = xi;
           f->center_bond = m + 1;
+          if (observer) flush_qr();  // the observer sees this gate's report
         } else {
           // Hastings-only scheme: the center matrix stays put; b_m is renormalized
           // by 1/sqrt(1 - eps) unless skip_renormalize (gates.cpp:564-571)
@@ -1261,6 +1268,10 @@ qt_status qt_finite_step(qt_finite* f, uint64_t n_layers, const int32_t* parity,
           f->sites[m] = o.b_m;
           f->sites[m + 1] = o.b_n;
         }
+        // FiniteGateObserver, proj/include/qrtebd/gates.hpp:120-123: after
+        // every gate, with the state as it stands
+        if (observer && observer(user, &out.back()) != 0)
+          throw qt::Error(qt::Err::internal, "gate observer failed");
       }
     }
     flush_qr();

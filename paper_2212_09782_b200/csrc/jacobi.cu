@@ -579,9 +579,27 @@ __global__ void jacobi_gather_kernel(const double2* __restrict__ V, int n, int N
   }
 }
 
-__global__ void sqrt_clip_kernel(const double* __restrict__ w, int n, double* s) {
+// s = sqrt(max(w, 0)) (Gram eigenvalues) or max(w, 0) (Jordan-Wielandt)
+__global__ void sqrt_clip_kernel(const double* __restrict__ w, int n, double* s, bool no_sqrt = false) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    s[i] = w[i] > 0.0 ? sqrt(w[i]) : 0.0;
+    s[i] = w[i] > 0.0 ? (no_sqrt ? w[i] : sqrt(w[i])) : 0.0;
+}
+
+// H = [[0, m], [m^H, 0]] ((p+q) x (p+q), row-major) for the p x q matrix m
+__global__ void jw_build_kernel(const double2* __restrict__ m, long long p, long long q, double2* __restrict__ h) {
+  const long long n = p + q, total = n * n;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = t / n, j = t % n;
+    double2 v = make_double2(0.0, 0.0);
+    if (i < p && j >= p) {
+      v = m[i * q + (j - p)];
+    } else if (i >= p && j < p) {
+      const double2 a = m[j * q + (i - p)];
+      v = make_double2(a.x, -a.y);
+    }
+    h[t] = v;
+  }
 }
 
 }  // namespace
@@ -806,53 +824,6 @@ __global__ void herm_defect_sum_kernel(const double* __restrict__ rows, int n, d
   }
 }
 
-// s_k^2 = || B[:, k] ||^2 over the rows of B (rows x k, ld k): one warp per
-// column, fixed lane order -> deterministic
-__global__ void colnorm2_kernel(const double2* __restrict__ b, long long rows, int k, double* s2) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= k) return;
-  double acc = 0.0;
-  for (long long r = lane; r < rows; r += 32) {
-    const double2 v = b[r * k + warp];
-    acc = fma(v.x, v.x, fma(v.y, v.y, acc));
-  }
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) s2[warp] = acc;
-}
-
-// s = sqrt(s2) sorted descending (ties: lower index first), one CTA bitonic
-__global__ void sqrt_sort_desc_kernel(const double* __restrict__ s2, int k, double* s) {
-  extern __shared__ unsigned char ssm[];
-  int P = 1;
-  while (P < k) P <<= 1;
-  double* key = reinterpret_cast<double*>(ssm);
-  int* idx = reinterpret_cast<int*>(key + P);
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    key[i] = i < k ? sqrt(fmax(s2[i], 0.0)) : -1.0;
-    idx[i] = i;
-  }
-  __syncthreads();
-  for (int size = 2; size <= P; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool desc = (i & size) == 0;
-          const bool i_first = (key[i] > key[j]) || (key[i] == key[j] && idx[i] < idx[j]);
-          if (desc != i_first) {
-            const double tk = key[i];
-            key[i] = key[j];
-            key[j] = tk;
-            const int ti = idx[i];
-            idx[i] = idx[j];
-            idx[j] = ti;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  for (int i = threadIdx.x; i < k; i += blockDim.x) s[i] = key[i];
-}
 }  // namespace
 
 
@@ -944,15 +915,21 @@ bool diagonal_singular_values(Engine& e, const double2* m, long long p, long lon
 }
 
 double* singular_values_device(Engine& e, const double2* m, long long p, long long q) {
-  // s = sqrt(max(eig(m^H m), 0)) (Gram route, absolute accuracy ~ sqrt(u) s_0
-  // for the smallest values), descending; returned in the S_EIG_W slot
+  // Singular values of Xi, descending (svd(Xi).s, proj/src/mps.cpp:198-207).
+  //  1. Gram route: s = sqrt(max(eig(m^H m), 0)).  Its absolute error is
+  //     ~u s_0^2 / s_k: exact enough (<= 1e-13 s_0) when the spectrum spans
+  //     less than 3 decades (s_min >= 1e-3 s_0) -- the common case.
+  //  2. Otherwise the Jordan-Wielandt matrix H = [[0, m], [m^H, 0]], whose
+  //     eigenvalues are +-s_k (and |p - q| zeros), goes through the same
+  //     backward-stable Jacobi eigensolver: every s_k to ~u s_0 absolute,
+  //     no squaring (|ds_k| <= 1e-10 s_0).
   const long long k = std::min(p, q);
   if (k == 0) return e.dbuf(S_EIG_W, 8);
-  double* wd = e.dbuf(S_EIG_W, k + 8);
+  double* wd = e.dbuf(S_EIG_W, std::max(k, p + q) + 8);
   if (diagonal_singular_values(e, m, p, q, wd)) return wd;
   const bool wide = q > p;  // Gram on the smaller side
   const long long g = wide ? p : q;
-  double2* gm = e.cbuf(S_GRAM, g * g);
+  double2* gm = e.cbuf(S_GRAM, std::max(g * g, (p + q) * (p + q)));
   GemmDesc d;
   d.M = g;
   d.N = g;
@@ -975,43 +952,33 @@ double* singular_values_device(Engine& e, const double2* m, long long p, long lo
   d.C = gm;
   d.ldc = g;
   zgemm(d, e.gemm_scratch(), e.stream);
-  double* w = e.dbuf(S_EIG_W, g + 8);
-  double2* v = e.cbuf(S_MISC2, g * g);
-  eigh_device(e, gm, g, w, v);
-  // Rayleigh-Ritz refinement: the Gram eigenvalues carry an absolute error
-  // ~u s_0^2, i.e. ~sqrt(u) s_0 in the small singular values; the Gram
-  // eigenvectors are accurate to ~u in angle, so the column norms of
-  // B = op(m) v (tall: m v; wide: m^H v) give every s_k to ~u s_0 absolute
-  // (|ds_k| <= 1e-10 s_0), then sort descending
-  const long long rows = wide ? q : p;
-  double2* bm = e.cbuf(S_QR_W, rows * g);
-  GemmDesc r;
-  r.M = rows;
-  r.N = g;
-  r.K = g;
-  r.opA = wide ? Op::H : Op::N;
-  r.A = m;
-  r.lda = q;
-  r.opB = Op::N;
-  r.B = v;
-  r.ldb = g;
-  r.C = bm;
-  r.ldc = g;
-  zgemm(r, e.gemm_scratch(), e.stream);
-  double* s2 = e.dbuf(S_MISC, g + 8);
-  colnorm2_kernel<<<static_cast<int>(ceil_div(g * 32, 256)), 256, 0, e.stream>>>(bm, rows, static_cast<int>(g), s2);
+  double2* v = e.cbuf(S_MISC2, std::max(g * g, (p + q) * (p + q)));
+  const EighStatus* st = eigh_device(e, gm, g, wd, v);
+  EighStatus hs{1, 0, 0.0, 0.0};
+  double ends[2] = {0.0, 0.0};
+  QT_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaMemcpyAsync(&ends[0], wd, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaMemcpyAsync(&ends[1], wd + (k - 1), sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  require_eigh_converged(hs, g);
+  const long long n2 = p + q;
+  if (ends[1] >= 1e-6 * ends[0] || n2 > 8192) {
+    sqrt_clip_kernel<<<1, 256, 0, e.stream>>>(wd, static_cast<int>(k), wd);
+    QT_LAUNCHED();
+    return wd;
+  }
+  jw_build_kernel<<<static_cast<int>(std::min<long long>(ceil_div(n2 * n2, 256), 8 * e.num_sms)), 256, 0,
+                    e.stream>>>(m, p, q, gm);
   QT_LAUNCHED();
-  int P = 1;
-  while (P < k) P <<= 1;
-  const size_t smem = static_cast<size_t>(P) * (sizeof(double) + sizeof(int));
-  if (smem > 200 * 1024) throw Error(Err::capacity, "schmidt_values: matrix too large for the device sort");
-  static std::once_flag once;
-  std::call_once(once, [] {
-    QT_CUDA(cudaFuncSetAttribute(sqrt_sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  });
-  sqrt_sort_desc_kernel<<<1, 1024, smem, e.stream>>>(s2, static_cast<int>(k), w);
+  st = eigh_device(e, gm, n2, wd, v);
+  QT_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, e.stream));
+  QT_CUDA(cudaStreamSynchronize(e.stream));
+  require_eigh_converged(hs, n2);
+  // the k largest eigenvalues are s_1 >= ... >= s_k >= 0 (rounding noise of
+  // exact zeros clipped)
+  sqrt_clip_kernel<<<1, 256, 0, e.stream>>>(wd, static_cast<int>(k), wd, true);
   QT_LAUNCHED();
-  return w;
+  return wd;
 }
 
 }  // namespace qt

@@ -1,5 +1,6 @@
-"""The C++ mirror header compiles against the C-ABI (CPU) and, on a B200,
-drives the device through the reference-shaped API (GPU)."""
+"""The reference-signature C++ API (include/qrtebd/qrtebd_api.hpp ->
+libqrtebd_api.so) compiles and links on CPU and, on a B200, drives the device
+with the reference's own call shapes (GPU)."""
 import os
 import subprocess
 
@@ -12,8 +13,8 @@ LIBDIR = os.path.join(ROOT, "paper_2212_09782_b200")
 
 
 def compile_cmd(out):
-    return ["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), SRC, "-o", out, "-L", LIBDIR,
-            "-lqrtebd_b200", f"-Wl,-rpath,{LIBDIR}"]
+    return ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), SRC, "-o", out, "-L", LIBDIR,
+            "-l:libqrtebd_api.so", f"-Wl,-rpath,{LIBDIR}"]
 
 
 def test_header_compiles_and_links(tmp_path):
