@@ -14,7 +14,7 @@ LIBDIR = os.path.join(ROOT, "paper_2212_09782_b200")
 
 def compile_cmd(out):
     return ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), SRC, "-o", out, "-L", LIBDIR,
-            "-l:libqrtebd_api.so", f"-Wl,-rpath,{LIBDIR}"]
+            "-l:libqrtebd_api.so", "-l:libqrtebd_b200.so", f"-Wl,-rpath,{LIBDIR}"]
 
 
 def test_header_compiles_and_links(tmp_path):
