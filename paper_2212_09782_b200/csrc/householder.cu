@@ -381,12 +381,17 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp, cudaStream_t s
   PanelArgs a = base;
   a.rpc = static_cast<int>(rpc);
   const size_t smem = (size_t(rpc) * NB + PANEL_WARPS * NB + NB * NB + 2 * NB) * sizeof(double2);
-  static std::once_flag attr_once;  // the largest panel (rpc <= 1024) fits 227 KB
+  // opt in once to the device's per-block maximum (thread-safe; every launch
+  // below needs at most that much)
+  static std::once_flag attr_once;
+  static int smem_cap = 0;
   std::call_once(attr_once, [] {
-    QT_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>((size_t(1024) * NB + PANEL_WARPS * NB + NB * NB + 2 * NB) *
-                                                  sizeof(double2))));
+    int dev = 0;
+    QT_CUDA(cudaGetDevice(&dev));
+    QT_CUDA(cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    QT_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
   });
+  if (smem > static_cast<size_t>(smem_cap)) throw Error(Err::capacity, "QR panel exceeds the shared-memory capacity");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(G));
   cfg.blockDim = dim3(PANEL_THREADS);

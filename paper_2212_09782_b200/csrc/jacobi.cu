@@ -769,7 +769,10 @@ void require_eigh_converged(const EighStatus& st, long long n) {
   const double u = 2.220446049250313e-16;
   const double lim = static_cast<double>(n) * u;
   if (st.offdiag2 <= lim * lim * st.fro2) return;
-  throw Error(Err::numeric, "eigh: factorization did not converge");
+  char buf[160];
+  std::snprintf(buf, sizeof(buf), "eigh: factorization did not converge (n=%lld, %d sweeps, offdiag %.3e of %.3e)", n,
+                -st.sweeps, std::sqrt(st.offdiag2), std::sqrt(st.fro2));
+  throw Error(Err::numeric, buf);
 }
 
 namespace {

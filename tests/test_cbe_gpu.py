@@ -217,6 +217,12 @@ def test_uniform_cbe_trajectory_matches_oracle(ctx, d, chi_max, steps):
             assert abs(zd - zo) <= 1e-10
             so = ref.schmidt_values(st_o, s)
             sd = q.schmidt_values(st_d, s, ctx)
-            assert len(sd) == len(so)
-            assert np.max(np.abs(sd - so)) <= 1e-10 * so[0]
+            # the reference keeps CBE Schmidt values from eigh(L^H L)
+            # (gates.cpp:408-419): values below ~sqrt(u) s_0 are rounding noise
+            # there (they can clip to 0 and fall under sv_cutoff), so the kept
+            # count may differ only by values under that floor
+            m = min(len(sd), len(so))
+            floor = 1e-7 * so[0]
+            assert np.all(sd[m:] < floor) and np.all(so[m:] < floor)
+            assert np.max(np.abs(sd[:m] - so[:m])) <= 1e-10 * so[0]
             assert abs(q.entropy_from_schmidt(sd) - ref.entropy_from_schmidt(so)) < 1e-10
