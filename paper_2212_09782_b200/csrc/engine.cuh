@@ -52,6 +52,8 @@ enum Slot : int {
   S_GEMM_PARTS,  // split-K scratch of GEMMs on e.side
   S_TILE_SUMSS,
   S_TILE_SUMS3,
+  S_QR_TOB,      // combined T factors of the outer (multi-panel) blocks of a tall QR
+  S_QR_GRAM,     // V_ob^H V_ob of one outer block, and the Z scratch of the T combination
   S_COUNT
 };
 

@@ -548,9 +548,12 @@ void apply_cols(const double2* Vp, long long ldv, const double2* Tp, int nbp, do
 
 // C <- H_p^H C = C - V T^H (V^H C) on stream st (three DMMA GEMMs; W/W2 and the
 // split-K scratch belong to that stream)
+// C <- (I - V T' V^H) C for a block of nbp reflectors, T' = T^H (Q^H C, the
+// factorization) or T (Q C, Q formation); T has leading dimension ldt
 void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, double2* C, long long ldc,
                            long long mp, long long nc, int nbp, double2* W, double2* W2, const GemmScratch& gs,
-                           cudaStream_t st, const std::function<void()>& after_top = nullptr) {
+                           cudaStream_t st, const std::function<void()>& after_top = nullptr, long long ldt = NB,
+                           bool t_adjoint = true) {
   GemmDesc g;
   g.M = nbp; g.N = nc; g.K = mp;
   g.opA = Op::H; g.A = Vp; g.lda = ldv;
@@ -559,7 +562,7 @@ void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, 
   zgemm(g, gs, st);
   GemmDesc g2;
   g2.M = nbp; g2.N = nc; g2.K = nbp;
-  g2.opA = Op::H; g2.A = Tp; g2.lda = NB;
+  g2.opA = t_adjoint ? Op::H : Op::N; g2.A = Tp; g2.lda = ldt;
   g2.opB = Op::N; g2.B = W; g2.ldb = nc;
   g2.C = W2; g2.ldc = nc;
   zgemm(g2, gs, st);
@@ -585,10 +588,205 @@ void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, 
 
 }  // namespace
 
+namespace {
+// T_ob (ob x ob, ld ob) of an outer block of npb panels starting at column J:
+// zero, with the panels' T factors (NB x NB each, the valid nbp x nbp part)
+// on the diagonal blocks
+__global__ void tob_init_kernel(const double2* __restrict__ T, long long J, long long k, int npb, double2* tob,
+                                int ob) {
+  const int total = ob * ob;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int i = t / ob, j = t % ob, p = i / NB;
+    double2 v = make_double2(0.0, 0.0);
+    if (j / NB == p && p < npb) {
+      const long long nbp = std::min<long long>(NB, k - J - static_cast<long long>(p) * NB);
+      const int ii = i % NB, jj = j % NB;
+      if (ii < nbp && jj < nbp) v = T[(static_cast<long long>(J / NB) + p) * NB * NB + ii * NB + jj];
+    }
+    tob[t] = v;
+  }
+}
+
+int qr_outer_width() {
+  static const int ob = [] {
+    const char* s = std::getenv("QT_QR_OB");
+    const int v = s ? std::atoi(s) : 128;
+    return v >= 64 && v % NB == 0 && v <= 512 ? v : (v == 0 ? 0 : 128);
+  }();
+  return ob;
+}
+
+}  // namespace
+
+// Tall QR (panels beyond one block-reflector cluster, m > 2048): two-level
+// blocking.  Panels of NB = 32 columns are factored inside outer blocks of OB
+// columns (QT_QR_OB, default 128), each panel's reflector reaching only the
+// rest of its outer block (narrow GEMMs); then the OB reflectors of the block
+// are combined into one compact-WY pair (V_ob, T_ob):
+//   T_ob = [[T_prev, -T_prev (V_prev^H V_c) T_c], [0, T_c]]   (panel by panel)
+// and the trailing matrix -- and, in Q formation, Q -- is updated with K = OB
+// DMMA GEMMs instead of K = 32 ones.  Look-ahead: the next outer block's
+// columns are updated on the main stream, the rest on e.side while the next
+// block's panels run; QrOpts::capply applies (V_ob, T_ob) to C on e.side2.
+void qr_inplace_outer(Engine& e, double2* a, long long m, long long n, long long lda, double2* q, long long ldq,
+                      double2* r, long long ldr, const QrOpts& opts) {
+  const long long k = std::min(m, n);
+  const int OB = qr_outer_width();
+  const long long npan = ceil_div(k, NB);
+  const long long kp = npan * NB;
+  const long long nob = ceil_div(k, static_cast<long long>(OB));
+  double2* V = e.cbuf(S_QR_V, static_cast<size_t>(m) * kp);
+  double2* T = e.cbuf(S_QR_T, static_cast<size_t>(npan) * NB * NB);
+  double2* TOB = e.cbuf(S_QR_TOB, static_cast<size_t>(nob) * OB * OB);
+  double2* G = e.cbuf(S_QR_GRAM, static_cast<size_t>(OB) * OB + static_cast<size_t>(OB) * NB);
+  double2* Z = G + static_cast<size_t>(OB) * OB;
+  double2* W = e.cbuf(S_QR_W, static_cast<size_t>(OB) * n);
+  double2* W2 = e.cbuf(S_QR_W2, static_cast<size_t>(OB) * n);
+  double2* SW = e.cbuf(S_QR_WS, static_cast<size_t>(OB) * n);
+  double2* SW2 = e.cbuf(S_QR_WS2, static_cast<size_t>(OB) * n);
+  double2* part = e.cbuf(S_QR_PART, static_cast<size_t>(2) * kNumSMs * NB + 2 * NB);
+  const GemmScratch gs = e.gemm_scratch();
+  GemmScratch gss;
+  gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
+  gss.partial_elems = size_t(1) << 22;
+  gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
+  gss.tile_sums_elems = size_t(1) << 16;
+  const bool capply = opts.capply != nullptr && opts.nc > 0;
+  double2 *CW = nullptr, *CW2 = nullptr;
+  GemmScratch gs2;
+  if (capply) {
+    CW = e.cbuf(S_QA_W, static_cast<size_t>(OB) * opts.nc);
+    CW2 = e.cbuf(S_QA_W2, static_cast<size_t>(OB) * opts.nc);
+    gs2 = e.gemm_scratch2();
+  }
+  PanelArgs base{};
+  base.lda = lda;
+  base.ldv = kp;
+  base.part = part;
+  base.diag = part + 2 * kNumSMs * NB;
+  base.bar = e.barrier;
+  base.dbg = nullptr;
+
+  // event ids: 3000 + 2b (T_ob(b) ready), 3001 + 2b (side update of block b done)
+  const size_t ev0 = 3000;
+  long long side_last = -1;
+  for (long long b = 0; b < nob; ++b) {
+    const long long J = b * OB;
+    const long long w = std::min<long long>(OB, k - J);  // reflectors in this block
+    const long long mb = m - J;
+    const int npb = static_cast<int>(ceil_div(w, NB));
+    // V's block rows [J, J + w) x cols [J, J + w): zero above each panel's own
+    // rows (the panels write their unit-lower triangles and everything below)
+    QT_CUDA(cudaMemset2DAsync(V + J * kp + J, kp * sizeof(double2), 0, w * sizeof(double2), w, e.stream));
+    for (int c = 0; c < npb; ++c) {
+      const long long j = J + static_cast<long long>(c) * NB;
+      const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+      const long long mp = m - j;
+      PanelArgs pa = base;
+      pa.A = a + j * lda + j;
+      pa.mp = mp;
+      pa.nbp = nbp;
+      pa.V = V + j * kp + j;
+      pa.T = T + (j / NB) * NB * NB;
+      launch_panel(e, pa, mp);
+      // inner update: the rest of this outer block only
+      const long long ninner = J + w - (j + nbp);
+      if (ninner > 0)
+        apply_block_reflector(pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, ninner, nbp, W, W2, gs, e.stream);
+    }
+    // T_ob: Gram of the block's reflectors, then the off-diagonal blocks
+    double2* Tb = TOB + b * OB * OB;
+    const double2* Vb = V + J * kp + J;
+    tob_init_kernel<<<static_cast<int>(ceil_div(static_cast<long long>(OB) * OB, 256)), 256, 0, e.stream>>>(
+        T, J, k, npb, Tb, OB);
+    QT_LAUNCHED();
+    if (npb > 1) {
+      GemmDesc gg;
+      gg.M = w; gg.N = w; gg.K = mb;
+      gg.opA = Op::H; gg.A = Vb; gg.lda = kp;
+      gg.opB = Op::N; gg.B = Vb; gg.ldb = kp;
+      gg.C = G; gg.ldc = OB;
+      zgemm(gg, gs, e.stream);
+      for (int c = 1; c < npb; ++c) {
+        const long long c0 = static_cast<long long>(c) * NB;
+        const long long nbc = std::min<long long>(NB, w - c0);
+        GemmDesc gz;  // Z = (V_prev^H V_c) T_c
+        gz.M = c0; gz.N = nbc; gz.K = nbc;
+        gz.A = G + c0; gz.lda = OB;
+        gz.B = T + (J / NB + c) * NB * NB; gz.ldb = NB;
+        gz.C = Z; gz.ldc = NB;
+        zgemm(gz, gs, e.stream);
+        GemmDesc gx;  // T_ob[0:c0, c0:c0+nbc] = -T_prev Z
+        gx.M = c0; gx.N = nbc; gx.K = c0;
+        gx.A = Tb; gx.lda = OB;
+        gx.B = Z; gx.ldb = NB;
+        gx.C = Tb + c0; gx.ldc = OB;
+        gx.alpha = -1.0; gx.beta = 0.0;
+        zgemm(gx, gs, e.stream);
+      }
+    }
+    if (capply) {  // C <- Q_ob^H C on side2, behind this block
+      QT_CUDA(cudaEventRecord(e.event(ev0 + 2 * b), e.stream));
+      QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(ev0 + 2 * b), 0));
+      apply_block_reflector(Vb, kp, Tb, opts.capply + J * opts.ldc, opts.ldc, mb, opts.nc, static_cast<int>(w), CW,
+                            CW2, gs2, e.side2, nullptr, OB, true);
+    }
+    const long long ntr = n - (J + w);
+    if (ntr <= 0) continue;
+    // look-ahead: the next block's columns on the main stream (after the side
+    // stream's update of the previous block reached them), the rest on e.side
+    const long long nn = std::min<long long>(OB, ntr);
+    if (side_last >= 0) QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(ev0 + 2 * side_last + 1), 0));
+    if (ntr > nn) {
+      if (!capply) QT_CUDA(cudaEventRecord(e.event(ev0 + 2 * b), e.stream));
+      QT_CUDA(cudaStreamWaitEvent(e.side, e.event(ev0 + 2 * b), 0));
+    }
+    apply_block_reflector(Vb, kp, Tb, a + J * lda + J + w, lda, mb, nn, static_cast<int>(w), W, W2, gs, e.stream,
+                          nullptr, OB, true);
+    if (ntr > nn) {
+      apply_block_reflector(Vb, kp, Tb, a + J * lda + J + w + nn, lda, mb, ntr - nn, static_cast<int>(w), SW, SW2,
+                            gss, e.side, nullptr, OB, true);
+      QT_CUDA(cudaEventRecord(e.event(ev0 + 2 * b + 1), e.side));
+      side_last = b;
+    }
+  }
+  if (side_last >= 0) QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(ev0 + 2 * side_last + 1), 0));
+  if (capply) {  // join side2: Q^H C complete
+    QT_CUDA(cudaEventRecord(e.event(ev0 + 2 * nob + 2), e.side2));
+    QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(ev0 + 2 * nob + 2), 0));
+  }
+  if (opts.want_q) {
+    // explicit thin Q = Q_ob(0) ... Q_ob(nob-1) I[:, :k], outer blocks backward
+    set_identity(e, q, m, k, ldq);
+    for (long long b = nob - 1; b >= 0; --b) {
+      const long long J = b * OB;
+      const long long w = std::min<long long>(OB, k - J);
+      apply_block_reflector(V + J * kp + J, kp, TOB + b * OB * OB, q + J * ldq + J, ldq, m - J, k - J,
+                            static_cast<int>(w), W, W2, gs, e.stream, nullptr, OB, false);
+    }
+    gauge_q_kernel<<<grid_for(m * k), 256, 0, e.stream>>>(a, lda, q, ldq, m, k);
+    QT_LAUNCHED();
+  }
+  if (opts.want_r) {
+    gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
+    QT_LAUNCHED();
+  }
+}
+
+namespace {
+bool use_outer_qr(long long m, long long k) {
+  return qr_outer_width() > 0 && !larfb_cluster_fits(m) && k > NB;
+}
+}  // namespace
+
 void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, double2* q, long long ldq,
                 double2* r, long long ldr, const QrOpts& opts) {
   const long long k = std::min(m, n);
   if (k == 0) return;
+  if (use_outer_qr(m, k)) {
+    qr_inplace_outer(e, a, m, n, lda, q, ldq, r, ldr, opts);
+    return;
+  }
   const long long npan = ceil_div(k, NB);
   const long long kp = npan * NB;
   double2* V = e.cbuf(S_QR_V, static_cast<size_t>(m) * kp);

@@ -767,7 +767,7 @@ void require_eigh_converged(const EighStatus& st, long long n) {
   // level of a backward-stable solver (n u ||G||_F)
   if (st.sweeps > 0) return;
   const double u = 2.220446049250313e-16;
-  const double lim = static_cast<double>(n) * u;
+  const double lim = 32.0 * static_cast<double>(n) * u;  // Jacobi's rounding floor, with margin
   if (st.offdiag2 <= lim * lim * st.fro2) return;
   char buf[160];
   std::snprintf(buf, sizeof(buf), "eigh: factorization did not converge (n=%lld, %d sweeps, offdiag %.3e of %.3e)", n,

@@ -25,7 +25,10 @@ def test_qr_known_answer(ctx):
                                  (1, 1), (3, 1), (2000, 65),
                                  # tall panels: GEMM block reflectors (m > 2048), the register panel at
                                  # 14/20 rows per warp, and the grid-barrier panel (m > 5120)
-                                 (3000, 40), (5120, 36), (6000, 40)])
+                                 (3000, 40), (5120, 36), (6000, 40),
+                                 # two-level blocking (outer blocks of 128 columns, m > 2048): several
+                                 # outer blocks, a ragged last panel and outer block, the look-ahead split
+                                 (3000, 300), (2100, 2100), (5120, 520), (2600, 129)])
 def test_qr_matches_oracle(ctx, m, n):
     rng = np.random.default_rng(m * 31 + n)
     a = crand(rng, m, n)
