@@ -225,14 +225,18 @@ void gemm(Engine& e, Op oa, Op ob, long long M, long long N, long long K, const 
 }  // namespace
 
 bool use_qtheta(const Engine& e, const qt_policy& pol, long long rows) {
-  // above ~2048 rows the extra reflector flops on theta outweigh the shorter
-  // critical path (north star: GEMM-bound); from 128 rows the pair pays for a
-  // lone update chain (C1, 128 rows: 771 -> 877 steps/s) but not when eight
-  // bond chains already share the GPU (C5-small, 192 rows: 183 -> 155 steps/s;
-  // QT_QTHETA_MIN_ROWS=256 restores that)
-  static const long long qtheta_max = std::getenv("QT_QTHETA_MAX_ROWS")
-                                          ? std::atoll(std::getenv("QT_QTHETA_MAX_ROWS"))
-                                          : 2048;
+  // Y = Q_m^H theta by applying QR(X)'s reflectors to theta (no explicit Q_m):
+  //  * up to 2048 rows: the pipelined pair (latency-bound chains); from 128
+  //    rows it pays for a lone update chain (C1, 128 rows: 771 -> 877 steps/s)
+  //    but not when eight bond chains already share the GPU (C5-small, 192
+  //    rows: 183 -> 155 steps/s; QT_QTHETA_MIN_ROWS=256 restores that);
+  //  * taller, with the explicit error on: the application (2 m eta n CMAC,
+  //    128-column outer blocks) replaces both the Y GEMM and the theta-sized
+  //    residual GEMM and drops Q_m's formation (north star 5.38 -> 5.84
+  //    steps/s, C3 1.257 -> 1.293, C5 0.376 -> 0.389); with the explicit error
+  //    off it would double the Y GEMM's flops (C4: 0.129 -> 0.117), so no
+  static const long long env_max = std::getenv("QT_QTHETA_MAX_ROWS") ? std::atoll(std::getenv("QT_QTHETA_MAX_ROWS")) : -1;
+  const long long qtheta_max = env_max >= 0 ? env_max : (pol.compute_explicit_error ? (1LL << 40) : 2048);
   static const long long qtheta_min = std::getenv("QT_QTHETA_MIN_ROWS")
                                           ? std::atoll(std::getenv("QT_QTHETA_MIN_ROWS"))
                                           : 128;
