@@ -160,6 +160,10 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 // heights within one block-reflector cluster (qr_pair_fits).  Everything is
 // joined into e.stream on return.
 bool qr_pair_fits(long long m, long long nc);
+// After qr_pair_pipelined: the explicit, gauge-fixed thin Q of X (m x k, ld
+// ldq) from the reflectors the pair left in S_QR_V / S_QR_T, on stream st
+// (left_iso of apply_gate_qr, proj/src/gates.cpp:373)
+void pair_form_q(Engine& e, const double2* x, long long m, long long k, double2* q, long long ldq, cudaStream_t st);
 // on_qblock (optional): called on the Q stream once columns [c0, c0 + nb) of
 // qy are formed and gauge-fixed (consumers of Q start behind the Y chain).
 // Callers may leave work in flight on e.side (the X look-ahead stream: X's

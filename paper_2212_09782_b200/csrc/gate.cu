@@ -378,7 +378,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   // afterwards.  Measured no faster at C2 (194 vs 196 steps/s: the theta GEMM
   // shares the SMs with X and the first panel), so off by default
   static const bool reassoc = std::getenv("QT_X_REASSOC") != nullptr;
-  const bool pair = qtheta && !out.left_iso && use_qr_pair(rows, cols);
+  const bool pair = qtheta && use_qr_pair(rows, cols);
   const bool x_reassoc = reassoc && pair && eta == cn && sweeps == 1;
   // Y0 = B^n regrouped (gates.cpp:357-361) on e.side while theta is built
   const bool y0_early = (eta == cn) && e.side != nullptr;
@@ -423,6 +423,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   // is wanted), no theta^H Q_m GEMM, and the explicit error needs only
   // ||Y - L Q_n||^2 + ||Z||^2 instead of a theta-sized residual product
   bool hastings_done = false;
+  bool left_pending = false;  // left_iso formed on side4 (pair path), joined at the end
   if (x_reassoc) {
     // theta on the theta stream (side2), behind phiev
     QT_CUDA(cudaEventRecord(e.event(0), e.stream));
@@ -453,7 +454,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     }
     if (!x_split) check_finite(e, X, rows * eta, flag);  // require_finite_matrix, linalg.cpp:17-21
     ustamp("X");
-    if (qtheta && !out.left_iso && use_qr_pair(rows, cols)) {
+    if (pair) {
       // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
       // QT_QB_HASTINGS=1: the Hastings columns of B~m follow the Q blocks of
       // Y^H (column block b of B~m = phiev Qp[:, b] as soon as that block of Qp
@@ -492,6 +493,18 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
           [&](long long r0, long long nr, cudaStream_t st) { qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st); },
           hastings_block);
       hastings_done = static_cast<bool>(hastings_block);
+      if (out.left_iso) {
+        // left_iso = Q_m (gates.cpp:373) from X's stored reflectors, on side4
+        // concurrently with the tail (Hastings on the main stream)
+        QT_CUDA(cudaEventRecord(e.event(1006), e.stream));
+        QT_CUDA(cudaStreamWaitEvent(e.side4, e.event(1006), 0));
+        pair_form_q(e, X, rows, eta, Qm, eta, e.side4);
+        const long long shp[3] = {cl, d, eta};
+        const int perm[3] = {1, 0, 2};
+        permute(e, Qm, 3, shp, perm, false, out.left_iso, 1.0, nullptr, e.side4);
+        QT_CUDA(cudaEventRecord(e.event(1007), e.side4));
+        left_pending = true;
+      }
       check_finite(e, theta, eta * cols, flag);  // Y (the first eta rows of Q_full^H theta)
       if (x_reassoc) norm2(e, theta, rows, cols, cols, e.dscal + SC_THETA2);  // ||Q_full^H theta|| = ||theta||
       ustamp("pair");
@@ -506,12 +519,14 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
       o.want_r = false;
       qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta, o);
       qtheta_yh(e, theta, cols, X, eta, YH);
+      ustamp("qrx_apply");
     } else {
       qr_inplace(e, X, rows, eta, eta, Qm, eta, Rm, eta);
       gemm(e, Op::H, Op::N, cols, eta, rows, theta, cols, Qm, eta, YH, eta);  // Y^H = theta^H Q_m
     }
     check_finite(e, YH, cols * eta, flag);
     qr_inplace(e, YH, cols, eta, eta, Qp, eta, Rp, eta);  // Y^H = Qp Rp -> L = Rp^H, Q_n = Qp^H
+    ustamp("qry");
   }
   norm2(e, Rp, eta, eta, eta, e.dscal + SC_L2);
   inv_norm_kernel<<<1, 1, 0, e.stream>>>(e.dscal, SC_THETA2, SC_L2, pol.skip_renormalize ? 1 : 0, SC_TMP0);
@@ -563,7 +578,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     g.C = out.b_m; g.ldc = cm * eta; g.rsplit = d; g.ldc_hi = eta;
     zgemm(g, e.gemm_scratch(), e.stream);
   }
-  if (out.left_iso) {
+  if (out.left_iso && !left_pending) {
     // left_iso = Q_m (cl, d, eta) -> (d, cl, eta)   (gates.cpp:198-201)
     const long long shp[3] = {cl, d, eta};
     const int perm[3] = {1, 0, 2};
@@ -589,6 +604,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     g.mode = GemmMode::resid;
     zgemm(g, e.gemm_scratch(), e.stream, e.dscal + SC_RESID);
   }
+  if (left_pending) QT_CUDA(cudaStreamWaitEvent(e.stream, e.event(1007), 0));
   ustamp("end");
   if (udbg) {
     QT_CUDA(cudaStreamSynchronize(e.stream));

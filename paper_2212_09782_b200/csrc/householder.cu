@@ -989,6 +989,25 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 
 bool qr_pair_fits(long long m, long long nc) { return larfb_cluster_fits(m) && larfb_cluster_fits(nc); }
 
+void pair_form_q(Engine& e, const double2* x, long long m, long long k, double2* q, long long ldq, cudaStream_t st) {
+  // Q = H_0 ... H_{k-1} I[:, :k] from QR(X)'s reflectors as the pair left them
+  // (S_QR_V / S_QR_T, leading dimension kp), block reflectors backward in one
+  // cluster launch each, then the gauge phases of X's diagonal
+  const long long npan = ceil_div(k, NB);
+  const long long kp = npan * NB;
+  const double2* V = e.cbuf(S_QR_V, static_cast<size_t>(m) * kp);
+  const double2* T = e.cbuf(S_QR_T, static_cast<size_t>(npan) * NB * NB);
+  set_identity(e, q, m, k, ldq, st);
+  for (long long p = npan - 1; p >= 0; --p) {
+    const long long j = p * NB;
+    const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+    if (!larfb_cluster(e, V + j * kp + j, kp, T + p * NB * NB, q + j * ldq + j, ldq, m - j, k - j, nbp, false, st))
+      throw Error(Err::internal, "pair_form_q: block reflector does not fit one cluster");
+  }
+  gauge_q_kernel<<<grid_for(m * k), 256, 0, st>>>(x, k, q, ldq, m, k);
+  QT_LAUNCHED();
+}
+
 namespace {
 // the cluster panel for mp rows would run with <= 5 rows per warp (fused look-ahead)
 bool panel_pre_fits(long long mp) {

@@ -177,3 +177,24 @@ def test_pair_nonfinite_input_is_input_error(ctx, where):
     o = ref.apply_gate_qr(xi, bm, bn, gate, ref.TruncationPolicy(**pol))
     upd = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=False)
     compare(upd, o, xi)
+
+
+@pytest.mark.parametrize("d,chi,chi_max", [(5, 64, 64), (5, 256, 256), (4, 96, 70), (3, 128, 188)])
+def test_pair_with_left_iso_matches_oracle(ctx, d, chi, chi_max):
+    """The reference signature always returns left_iso for qr (gates.cpp:373):
+    the pipelined pair keeps running and forms Q_m from QR(X)'s stored
+    reflectors beside the tail; Q_m is gauge-fixed, so left_iso is compared
+    directly (Appendix B (vi)), and the rest equals the left_iso-free update
+    bitwise."""
+    xi, bm, bn = random_inputs(d, chi, seed=55 * d + chi)
+    gate = model.make_gate(model.bond_hamiltonian(d, 2.0), 0.05)
+    pol = dict(chi_max=chi_max, sv_cutoff=1e-14, delta_chi_abs=max(0, chi_max - chi), delta_chi_rel=0.0)
+    o = ref.apply_gate_qr(xi, bm, bn, gate, ref.TruncationPolicy(**pol))
+    upd = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=True)
+    compare(upd, o, xi)
+    li = upd.left_iso.numpy()
+    assert np.linalg.norm(li - o.left_iso) / np.linalg.norm(o.left_iso) < 1e-10
+    plain = q.apply_gate_qr(xi, bm, bn, gate, q.TruncationPolicy(**pol), ctx, want_left_iso=False)
+    assert np.array_equal(plain.b_n.numpy(), upd.b_n.numpy())
+    assert np.array_equal(plain.b_m.numpy(), upd.b_m.numpy())
+    assert plain.report.eps_trunc == upd.report.eps_trunc
