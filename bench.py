@@ -320,44 +320,51 @@ def chain_config_dict(cc, ws):
             "l2": "chain state (GBs) far larger than L2"}
 
 
-def run_chain(args, cc):
-    """C5: finite chain in Hastings form, contiguous even-aligned site blocks
-    per rank; odd layers exchange the straddling boundary tensors with NCCL
-    send/recv (paper_2212_09782_b200/finite.py).  Strong scaling: the chain is
-    fixed, value = Trotter steps/s of the whole chain from the max over ranks."""
+def run_chain(args, cc, as_anchor=False):
+    """C5: finite chain in Hastings form through the C-ABI sharded chain
+    (qt_chain_*, qt_tebd_step_finite_sharded, csrc/chain.cu): contiguous
+    even-aligned site blocks per rank, interior bonds on 8 concurrent worker
+    contexts, the straddling tensors exchanged with ncclSend / ncclRecv of raw
+    device buffers (the NCCL id broadcast over torch.distributed).  Strong
+    scaling: the chain is fixed, value = Trotter steps/s of the whole chain
+    from the max over ranks.  as_anchor: return the line instead of printing
+    (the N=1 run's C5 point for a scaling curve)."""
     import torch
 
     from paper_2212_09782_b200 import _capi, model
     from paper_2212_09782_b200 import qrtebd as q
-    from paper_2212_09782_b200.finite import ShardedChain, chain_dims, device_backend, partition, random_chain_state
+    from paper_2212_09782_b200.chain import DeviceChain, nccl_unique_id, partition
+    from paper_2212_09782_b200.finite import chain_dims, random_chain_state
 
-    if args.impl == "reference":
+    if args.impl == "reference" and not as_anchor:
         return run_chain_reference(args, cc)
-    ws, rank, local = dist_setup()
+    ws, rank, local = (1, 0, 0) if as_anchor else dist_setup()
     import torch.distributed as dist_mod
-    dist = dist_mod if ws > 1 else None
     n, d, chi, scheme, explicit = cc["n"], cc["d"], cc["chi"], cc["scheme"], cc["explicit"]
     torch.cuda.set_device(local)
     ctx = _capi.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
     dmma_peak = ctx.fp64_peak(0)
-    start, end = partition(n, ws)[rank]
+    start, end = partition(n, ws, rank)
     sites, bonds, keep = random_chain_state(ctx, n, d, chi, start, end)
+    nid = None
+    if ws > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist_mod.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    workers = max(0, int(os.environ.get("QT_CHAIN_STREAMS", "8")))
+    chain = DeviceChain(ctx, n, sites, bonds, rank, ws, nccl_id=nid, workers=workers)
+    del sites, bonds, keep
     layers = []
     for parity, dte in model.layer_structure(0.05, 2):
         layers.append((0 if parity == "even" else 1,
                        [ctx.tensor(model.make_gate(model.chain_bond_hamiltonian(d, 2.0, m, n), dte))
-                        for m in range(n - 1)]))
+                        if start <= m + 1 and m < end else None for m in range(n - 1)]))
     pol = q.TruncationPolicy(chi_max=chi, delta_chi_abs=0, delta_chi_rel=0.0, compute_explicit_error=explicit)
-    # same-parity bonds run concurrently on `streams` contexts (one stream and
-    # workspace each) besides the exchange context
-    nstreams = max(0, int(os.environ.get("QT_CHAIN_STREAMS", "8")))
-    wctx = [_capi.Context(local) for _ in range(nstreams)]
-    backends = [device_backend(ctx, scheme, pol)] + [device_backend(c, scheme, pol) for c in wctx]
-    chain = ShardedChain(sites, bonds, n, rank, ws, backends, dist)
-    warmup = max(1, min(args.warmup, 2)) if args.steps <= 3 else args.warmup
+    steps = 2 if as_anchor else args.steps
+    warmup = 1 if as_anchor else (max(1, min(args.warmup, 2)) if args.steps <= 3 else args.warmup)
     for _ in range(warmup):
-        chain.step(layers, device=f"cuda:{local}")
+        chain.step(layers, scheme, pol)
     sampler = ClockSampler(local)
     sampler.start()
     barrier(ws)
@@ -365,10 +372,10 @@ def run_chain(args, cc):
     ctx.synchronize()
     launches0 = ctx.lib.qt_kernel_launches()
     step_ms = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        chain.step(layers, device=f"cuda:{local}")
+        chain.step(layers, scheme, pol)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -377,34 +384,37 @@ def run_chain(args, cc):
     clocks = sampler.stop()
     launches = ctx.lib.qt_kernel_launches() - launches0
     tot_ms = max_over_ranks(sum(step_ms), ws)
-    ms_per_step = tot_ms / args.steps
+    ms_per_step = tot_ms / steps
     chis = chain_dims(n, d, chi)
     f_step = 0.0
     for parity, _ in layers:
         for m in range(parity, n - 1, 2):
-            cm, cn, cr = chis[m], chis[m + 1], chis[m + 2]
-            eta = min(cn, cm * d, d * cr)
+            cn = chis[m + 1]
+            eta = min(cn, chis[m] * d, d * chis[m + 2])
             f_step += flops_per_update(d, cn, eta, eta, explicit)  # uniform-chi estimate per bond
     upd_per_step = sum(len(range(p, n - 1, 2)) for p, _ in layers)
     line = {
-        "metric": METRIC, "value": 1e3 / ms_per_step, "unit": "steps/s", "n_gpus": ws, "steps": args.steps,
+        "metric": METRIC, "value": 1e3 / ms_per_step, "unit": "steps/s", "n_gpus": ws, "steps": steps,
         "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
         "config": chain_config_dict(cc, ws),
+        "path": f"C-ABI qt_tebd_step_finite_sharded: {workers} worker contexts per rank, NCCL send/recv of the "
+                "straddling site tensors" if ws > 1 else f"C-ABI qt_tebd_step_finite_sharded, {workers} worker contexts",
         "updates_per_s": upd_per_step * 1e3 / ms_per_step,
         "step_ms": [round(x, 3) for x in step_ms],
-        "roofline": {"bound": "tensor", "achieved": f_step / (ms_per_step * 1e-3) / 1e12 * ws, "peak": dmma_peak * ws,
-                     "unit": "TFLOP/s", "frac": f_step / (ms_per_step * 1e-3) / 1e12 / dmma_peak,
-                     "traffic": None, "kernel": "whole step (all kernels), algorithmic flops / device time",
+        "roofline": {"bound": "tensor", "achieved": f_step / (ms_per_step * 1e-3) / 1e12, "peak": dmma_peak * ws,
+                     "unit": "TFLOP/s", "frac": f_step / (ms_per_step * 1e-3) / 1e12 / (dmma_peak * ws),
+                     "traffic": None, "scope": "whole chain step (all kernels), algorithmic flops / device time",
                      "flops_per_step": f_step},
         "gpu_launches": int(launches), "clocks": clocks,
     }
+    chain.close()
+    del layers
+    ctx.close()
+    if as_anchor:
+        return line
     if rank == 0:
         print(json.dumps(line), flush=True)
-    del chain, sites, bonds, keep, layers
-    for c in wctx:
-        c.close()
-    ctx.close()
     if ws > 1:
         dist_mod.destroy_process_group()
     return 0
@@ -482,6 +492,8 @@ def main():
                     help="default: north (N=1) / c5 sharded chain (N>1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scaling-anchor", action="store_true",
+                    help="skip the 1-GPU C5 chain point appended to the default N=1 line")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--path", default="graph", choices=["graph", "value"],
                     help="graph: device-resident state, CUDA-graph step; value: C-ABI tebd_step (new handles)")
@@ -664,11 +676,19 @@ def main():
             line["cpu_baseline_svd"] = {"value": rate_s, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                                         "sample": f"{n_s} updates ({dt_s:.1f} s) of the oracle's SVD-TEBD update "
                                                   "(zgesdd of theta) on the same state and gate schedule"}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     if graph_path:
         dev.close()
     ctx.close()
+    if rank == 0 and ws == 1 and not args.no_scaling_anchor:
+        # the N=1 point of the scaling curve: `bench.py --gpus N` (N > 1)
+        # runs the C5 chain sharded over N ranks; its 1-GPU value, measured
+        # here after the headline's timed region
+        a = run_chain(args, CHAIN_CONFIGS["c5"], as_anchor=True)
+        line["scaling_anchor"] = {"config": a["config"]["workload"], "n_gpus": 1, "value": a["value"],
+                                  "unit": a["unit"], "ms_per_step": a["ms_per_step"], "steps": a["steps"],
+                                  "roofline_frac": a["roofline"]["frac"], "path": a["path"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

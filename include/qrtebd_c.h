@@ -272,6 +272,42 @@ qt_status qt_left_defect(qt_ctx* ctx, const qt_tensor* b, double* out);
 qt_status qt_check_isometric_finite(const qt_finite* f, double tol, double* right_defects, double* left_defects,
                                     double* norm_defect, qt_isometry_report* out);
 
+/* ---- sharded finite chain (Hastings form), SURVEY.md §8(a) a10, §8(e) ------
+ * An open chain of n sites cut into contiguous, even-aligned site blocks, one
+ * per rank (process + GPU); the bond matrix Xi[m] sits left of site m (Xi[0] =
+ * [[1]]).  A layer of parity P updates every bond (m, m+1), m = P mod 2
+ * (proj/src/gates.cpp:513-540 without the wraparound); interior bonds run
+ * concurrently on n_workers worker contexts, and the bond straddling a block
+ * boundary is updated by the left rank after the right rank sent it its first
+ * site tensor (ncclSend / ncclRecv of raw device buffers on a dedicated
+ * stream; shapes travel in a small header first), Xi[e] and B[e] going back.
+ * The result is bitwise the single-rank chain's.  world == 1 needs no
+ * transport; world > 1 takes an NCCL unique id (qt_nccl_get_unique_id on
+ * rank 0, broadcast by the caller) or an in-process loopback shared by one
+ * chain per rank in separate host threads (tests on one GPU). */
+typedef struct qt_chain qt_chain;
+typedef struct qt_loopback qt_loopback;
+qt_status qt_nccl_get_unique_id(uint8_t* id128);
+qt_status qt_loopback_create(int world, qt_loopback** out);
+qt_status qt_loopback_destroy(qt_loopback* l);
+/* the owned sites [*begin, *end) of rank in world */
+qt_status qt_chain_partition(uint64_t n_sites, int world, int rank, uint64_t* begin, uint64_t* end);
+/* sites / bonds: the owned site tensors and the bond matrices left of them,
+ * indexed from *begin (copied) */
+qt_status qt_chain_create(qt_ctx* ctx, uint64_t n_sites, int rank, int world, const uint8_t* nccl_id,
+                          qt_loopback* loopback, qt_tensor* const* sites, qt_tensor* const* bonds, int n_workers,
+                          qt_chain** out);
+qt_status qt_chain_destroy(qt_chain* c);
+qt_status qt_chain_range(const qt_chain* c, uint64_t* begin, uint64_t* end);
+/* which: 0 = site tensor m, 1 = bond matrix left of site m (owned m; non-owning view) */
+qt_status qt_chain_view(qt_chain* c, int which, uint64_t m, qt_tensor** out);
+/* one Trotter step: layers[l] has parity parity[l] and gates[l * (n - 1) + m]
+ * on bond (m, m+1) (entries of bonds this rank does not update may be NULL);
+ * reports: this rank's updates, bond order per layer */
+qt_status qt_tebd_step_finite_sharded(qt_chain* c, uint64_t n_layers, const int32_t* parity, qt_tensor* const* gates,
+                                      qt_scheme scheme, const qt_policy* policy, qt_bond_report* reports,
+                                      uint64_t* n_reports);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Per-launch CUDA-event profile of the DMMA GEMM kernel (roofline evidence):
  * between begin and end every GEMM launch is bracketed by events; end

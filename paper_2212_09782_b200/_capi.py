@@ -116,6 +116,18 @@ SIGNATURES = {
     "qt_finite_step": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int, C.POINTER(qt_policy),
                                  C.POINTER(qt_bond_report), U64P]),
     "qt_finite_observables": (C.c_int, [P, P, DP, DP, C.c_uint64, U64P]),
+    "qt_finite_step_observed": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int, C.POINTER(qt_policy),
+                                          C.POINTER(qt_bond_report), U64P, P, P]),
+    "qt_nccl_get_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "qt_loopback_create": (C.c_int, [C.c_int, PP]),
+    "qt_loopback_destroy": (C.c_int, [P]),
+    "qt_chain_partition": (C.c_int, [C.c_uint64, C.c_int, C.c_int, U64P, U64P]),
+    "qt_chain_create": (C.c_int, [P, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint8), P, PP, PP, C.c_int, PP]),
+    "qt_chain_destroy": (C.c_int, [P]),
+    "qt_chain_range": (C.c_int, [P, U64P, U64P]),
+    "qt_chain_view": (C.c_int, [P, C.c_int, C.c_uint64, PP]),
+    "qt_tebd_step_finite_sharded": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int,
+                                              C.POINTER(qt_policy), C.POINTER(qt_bond_report), U64P]),
     "qt_left_defect": (C.c_int, [P, P, DP]),
     "qt_check_isometric_finite": (C.c_int, [P, C.c_double, DP, DP, DP, P]),
     "qt_expectation_local": (C.c_int, [P, P, P, P, DP]),

@@ -189,6 +189,9 @@ qt_policy policy_or_default(const qt_policy* p) {
 extern "C" {
 
 const char* qt_last_error(void) { return g_last_error.c_str(); }
+// internal (not in the public header): other translation units of the library
+// report errors through the same thread-local string
+void qt_internal_set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
 const char* qt_version(void) { return "qrtebd-b200 0.1.0 (sm_100a, complex128 DMMA)"; }
 
 void qt_policy_default(qt_policy* p) {

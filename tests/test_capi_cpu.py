@@ -73,3 +73,19 @@ def test_null_arguments_are_input_errors():
     lib = _capi.load()
     assert lib.qt_ctx_create(0, None, None) in (_capi.QT_ERR_INPUT, _capi.QT_ERR_CUDA)
     assert lib.qt_tensor_free(None) == _capi.QT_OK
+
+
+@pytest.mark.parametrize("n,world", [(2, 1), (8, 2), (9, 2), (256, 8), (10, 3), (6, 4), (255, 8)])
+def test_chain_partition_matches_host_logic(n, world):
+    """qt_chain_partition (the C-ABI sharded chain, csrc/chain.cu) cuts the
+    chain exactly as the host-side ShardedChain does (finite.partition):
+    contiguous, even-aligned blocks; an odd last site joins the last block."""
+    from paper_2212_09782_b200.chain import partition
+    from paper_2212_09782_b200.finite import partition as host_partition
+    blocks = host_partition(n, world)
+    for r in range(world):
+        b, e = partition(n, world, r)
+        if r < len(blocks):
+            assert (b, e) == blocks[r]
+        else:
+            assert b == e  # more ranks than site pairs: empty block
