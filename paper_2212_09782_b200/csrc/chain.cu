@@ -19,6 +19,7 @@
 // GPU for the multi-rank tests.  Results are committed in bond order, so a
 // sharded step is bitwise the single-rank step.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -54,8 +55,46 @@ void ok(qt_status s) {
 void cuda_ok(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw ChainError(QT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+// NCCL is resolved at first use (dlopen of libnccl.so.2), not at load time:
+// a process that imports torch after this library must still get torch's own
+// NCCL build, and when torch is already loaded the same soname resolves to
+// its copy -- one NCCL per process either way
+struct Nccl {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const Nccl& nccl() {
+  static const Nccl n = [] {
+    Nccl x;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw ChainError(QT_ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* name) {
+      void* p = dlsym(h, name);
+      if (!p) throw ChainError(QT_ERR_NCCL, std::string("libnccl.so.2 lacks ") + name);
+      return p;
+    };
+    x.get_unique_id = reinterpret_cast<decltype(x.get_unique_id)>(sym("ncclGetUniqueId"));
+    x.comm_init_rank = reinterpret_cast<decltype(x.comm_init_rank)>(sym("ncclCommInitRank"));
+    x.comm_destroy = reinterpret_cast<decltype(x.comm_destroy)>(sym("ncclCommDestroy"));
+    x.group_start = reinterpret_cast<decltype(x.group_start)>(sym("ncclGroupStart"));
+    x.group_end = reinterpret_cast<decltype(x.group_end)>(sym("ncclGroupEnd"));
+    x.send = reinterpret_cast<decltype(x.send)>(sym("ncclSend"));
+    x.recv = reinterpret_cast<decltype(x.recv)>(sym("ncclRecv"));
+    x.error_string = reinterpret_cast<decltype(x.error_string)>(sym("ncclGetErrorString"));
+    return x;
+  }();
+  return n;
+}
+
 void nccl_ok(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw ChainError(QT_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+  if (r != ncclSuccess) throw ChainError(QT_ERR_NCCL, std::string(what) + ": " + nccl().error_string(r));
 }
 
 // ---------------------------------------------------------------- transports
@@ -78,20 +117,20 @@ struct NcclTransport : Transport {
   };
   std::vector<Op> ops;
   ~NcclTransport() override {
-    if (comm) ncclCommDestroy(comm);
+    if (comm) nccl().comm_destroy(comm);
   }
   void group_start() override { ops.clear(); }
   void send(const void* buf, size_t bytes, int peer) override { ops.push_back({true, const_cast<void*>(buf), bytes, peer}); }
   void recv(void* buf, size_t bytes, int peer) override { ops.push_back({false, buf, bytes, peer}); }
   void group_end(cudaStream_t st) override {
-    nccl_ok(ncclGroupStart(), "ncclGroupStart");
+    nccl_ok(nccl().group_start(), "ncclGroupStart");
     for (const Op& o : ops) {
       if (o.is_send)
-        nccl_ok(ncclSend(o.buf, o.bytes, ncclUint8, o.peer, comm, st), "ncclSend");
+        nccl_ok(nccl().send(o.buf, o.bytes, ncclUint8, o.peer, comm, st), "ncclSend");
       else
-        nccl_ok(ncclRecv(o.buf, o.bytes, ncclUint8, o.peer, comm, st), "ncclRecv");
+        nccl_ok(nccl().recv(o.buf, o.bytes, ncclUint8, o.peer, comm, st), "ncclRecv");
     }
-    nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+    nccl_ok(nccl().group_end(), "ncclGroupEnd");
     ops.clear();
   }
 };
@@ -215,6 +254,9 @@ struct qt_chain {
   std::vector<qt_tensor*> sites;  // sites[m - begin]
   std::vector<qt_tensor*> bonds;  // bonds[m - begin]: the bond matrix left of site m
   std::vector<qt_ctx*> workers;
+  // the straddling bond's context: configured like the workers, so that every
+  // bond runs the same code path on every rank (bitwise the one-rank chain)
+  qt_ctx* edge = nullptr;
   cudaStream_t comm_stream = nullptr;
   std::unique_ptr<Transport> tr;
   // device scratch: headers (8 int64 each: out / in)
@@ -223,6 +265,7 @@ struct qt_chain {
     for (qt_tensor* t : sites) qt_tensor_free(t);
     for (qt_tensor* t : bonds) qt_tensor_free(t);
     for (qt_ctx* w : workers) qt_ctx_destroy(w);
+    if (edge) qt_ctx_destroy(edge);
     if (hdr) cudaFree(hdr);
     tr.reset();
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -314,7 +357,7 @@ qt_status qt_nccl_get_unique_id(uint8_t* id128) {
   return guard_chain([&] {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
     ncclUniqueId id;
-    nccl_ok(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    nccl_ok(nccl().get_unique_id(&id), "ncclGetUniqueId");
     std::memcpy(id128, &id, 128);
   });
 }
@@ -365,6 +408,10 @@ qt_status qt_chain_create(qt_ctx* ctx, uint64_t n_sites, int rank, int world, co
       ok(qt_ctx_set_qr_pair_min_rows(wc, 256));
       c->workers.push_back(wc);
     }
+    if (n_workers > 0) {
+      ok(qt_ctx_create(dev, nullptr, &c->edge));
+      ok(qt_ctx_set_qr_pair_min_rows(c->edge, 256));
+    }
     cuda_ok(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_ok(cudaMalloc(&c->hdr, 16 * sizeof(int64_t)), "cudaMalloc");
     if (world > 1) {
@@ -375,7 +422,7 @@ qt_status qt_chain_create(qt_ctx* ctx, uint64_t n_sites, int rank, int world, co
         auto t = std::make_unique<NcclTransport>();
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, 128);
-        nccl_ok(ncclCommInitRank(&t->comm, world, id, rank), "ncclCommInitRank");
+        nccl_ok(nccl().comm_init_rank(&t->comm, world, id, rank), "ncclCommInitRank");
         c->tr = std::move(t);
       }
     }
@@ -463,9 +510,10 @@ qt_status qt_tebd_step_finite_sharded(qt_chain* c, uint64_t n_layers, const int3
         for (auto& x : err)
           if (x) std::rethrow_exception(x);
       } else {
+        qt_ctx* ic = c->workers.empty() ? c->ctx : c->workers[0];
         for (size_t i = 0; i < inner.size(); ++i) {
           const uint64_t m = inner[i];
-          res[i] = update_on(c->ctx, scheme, bond(m), site(m), site(m + 1), gate(m), policy);
+          res[i] = update_on(ic, scheme, bond(m), site(m), site(m + 1), gate(m), policy);
         }
       }
       for (size_t i = 0; i < inner.size(); ++i) {
@@ -483,7 +531,8 @@ qt_status qt_tebd_step_finite_sharded(qt_chain* c, uint64_t n_layers, const int3
       if (right) {
         cuda_ok(cudaStreamSynchronize(c->comm_stream), "comm sync");  // B[e] arrived
         ok(qt_ctx_synchronize(c->ctx));
-        Upd u = update_on(c->ctx, scheme, bond(e - 1), site(e - 1), rsite, gate(e - 1), policy);
+        qt_ctx* ec = c->edge ? c->edge : c->ctx;
+        Upd u = update_on(ec, scheme, bond(e - 1), site(e - 1), rsite, gate(e - 1), policy);
         qt_tensor_free(site(e - 1));
         site(e - 1) = u.bm;
         rxi = u.xi;
