@@ -54,6 +54,7 @@ enum Slot : int {
   S_TILE_SUMS3,
   S_QR_TOB,      // combined T factors of the outer (multi-panel) blocks of a tall QR
   S_QR_GRAM,     // V_ob^H V_ob of one outer block, and the Z scratch of the T combination
+  S_QN,          // Q_n = Qp^H (eta x cols): the Hastings GEMM's B operand read K-major
   S_COUNT
 };
 

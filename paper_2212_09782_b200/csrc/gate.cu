@@ -576,6 +576,21 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     g.A = phiev; g.lda = cols;
     g.B = Qp; g.ldb = eta;
     g.C = out.b_m; g.ldc = cm * eta; g.rsplit = d; g.ldc_hi = eta;
+    // large products read B = Q_n^H from an explicit Q_n (op H, K-major
+    // fragments like the X GEMM) instead of Qp (op N): fewer shared-memory
+    // bank conflicts in the mainloop (north star: 86% -> 98% DMMA pipe active
+    // for X vs Hastings with the same grid)
+    static const int qn_env = std::getenv("QT_HASTINGS_QN") ? std::atoi(std::getenv("QT_HASTINGS_QN")) : -1;
+    const bool use_qn = qn_env >= 0 ? qn_env != 0 : (cm * d >= 2048 && cols >= 2048);
+    if (use_qn) {
+      double2* Qn = e.cbuf(S_QN, eta * cols);
+      const long long shp[2] = {cols, eta};
+      const int perm[2] = {1, 0};
+      permute(e, Qp, 2, shp, perm, true, Qn);
+      g.opB = Op::H;
+      g.B = Qn;
+      g.ldb = cols;
+    }
     zgemm(g, e.gemm_scratch(), e.stream);
   }
   if (out.left_iso && !left_pending) {

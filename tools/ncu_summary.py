@@ -28,34 +28,34 @@ METRICS = [
 
 
 def raw(path):
+    """Every profiled kernel of a report: [{metric: (value, unit)}]."""
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+    hdr, units = rows[0], rows[1]
+    return [{h: (v, u) for h, u, v in zip(hdr, units, vals)} for vals in rows[2:] if vals]
 
 
 def main():
     print(f"{'report':22s} {'kernel':44s} " + " ".join(f"{n:>12s}" for n, _ in METRICS))
     for path in sys.argv[1:]:
-        d = raw(path)
-        name = d.get("Kernel Name", ("?", ""))[0]
-        cells = []
-        for _, key in METRICS:
-            v, u = d.get(key, ("-", ""))
-            try:
-                x = float(v.replace(",", ""))
-                if u == "Mbyte" or u == "Gbyte" or u == "Kbyte" or u == "byte":
-                    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}[u]
-                    x *= scale
-                elif u == "ms":
-                    x *= 1e3
-                elif u == "ns":
-                    x *= 1e-3
-                cells.append(f"{x:12.4g}")
-            except ValueError:
-                cells.append(f"{v:>12s}")
-        print(f"{os.path.basename(path):22s} {name[:44]:44s} " + " ".join(cells))
-
+        for d in raw(path):
+            name = d.get("Kernel Name", ("?", ""))[0]
+            cells = []
+            for _, key in METRICS:
+                v, u = d.get(key, ("-", ""))
+                try:
+                    x = float(v.replace(",", ""))
+                    if u == "Mbyte" or u == "Gbyte" or u == "Kbyte" or u == "byte":
+                        scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}[u]
+                        x *= scale
+                    elif u == "ms":
+                        x *= 1e3
+                    elif u == "ns":
+                        x *= 1e-3
+                    cells.append(f"{x:12.4g}")
+                except ValueError:
+                    cells.append(f"{v:>12s}")
+            print(f"{os.path.basename(path):22s} {name[:44]:44s} " + " ".join(cells))
 
 if __name__ == "__main__":
     main()
