@@ -265,10 +265,42 @@ def cpu_reference_rate(cfg, budget_s, min_updates=1, warmup_updates=0, seed=0x51
         n += 1
         if n >= min_updates and time.perf_counter() - t0 >= budget_s:
             break
-        if time.perf_counter() - t0 >= 4 * budget_s:
+        if budget_s > 0 and time.perf_counter() - t0 >= 4 * budget_s:
             break
     dt = time.perf_counter() - t0
     return (n / 3.0) / dt, n, dt
+
+
+REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+
+
+def reference_binary_rate(cfg, budget_s, min_updates=1, scheme=None):
+    """The reference ITSELF on the host cores: oracle/_ref/ref_bench is
+    /root/reference/proj/src compiled in place on the Eigen-3.4-subset shim
+    over OpenBLAS (oracle/Makefile; test infrastructure, never the product).
+    It runs the reference's own apply_gate in tebd_step order on the same
+    synthetic state, with the reference's own gate construction, all host
+    threads.  Returns (steps/s, updates, seconds, threads) or None when the
+    binary is absent."""
+    import tempfile
+    if not os.access(REF_BENCH, os.X_OK):
+        return None
+    _, d, chi, cfg_scheme, explicit, (dabs, drel) = cfg
+    sites, bonds = synthetic_state(d, chi)
+    cores = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "state.bin")
+        with open(path, "wb") as f:
+            for a in sites + bonds:
+                f.write(np.ascontiguousarray(a, dtype=np.complex128).tobytes())
+        env = dict(os.environ, OMP_NUM_THREADS=str(cores), OPENBLAS_NUM_THREADS=str(cores))
+        out = subprocess.run([REF_BENCH, path, str(d), str(chi), scheme or cfg_scheme, "1" if explicit else "0",
+                              str(dabs), str(drel), str(budget_s), str(min_updates)], capture_output=True, text=True,
+                             env=env)
+    if out.returncode != 0:
+        raise RuntimeError(f"ref_bench failed: {out.stderr[-500:]}")
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    return (r["updates"] / 3.0) / r["seconds"], r["updates"], r["seconds"], r["threads"]
 
 
 def config_dict(cfg, ws):
@@ -291,18 +323,31 @@ def run_reference(args, cfg):
     # (north star: ~10 s per update on 16 cores) as many updates as fit in
     # the budget, at least one -- the whole run stays within a few minutes
     budget = float(os.environ.get("QT_REF_BUDGET_S", "60"))
-    warm = 1 if (args.warmup > 0 and chi <= 256) else 0
-    rate, n, dt = cpu_reference_rate(cfg, budget_s=budget if chi > 256 else 0.0,
-                                     min_updates=3 * max(1, args.steps) if chi <= 256 else 1, warmup_updates=warm)
+    kind = os.environ.get("QT_REF_IMPL", "reference")
+    refbin = reference_binary_rate(cfg, budget_s=budget if chi > 256 else 0.0,
+                                   min_updates=3 * max(1, args.steps) if chi <= 256 else 1) \
+        if kind == "reference" else None
+    if refbin is not None:
+        rate, n, dt, cores = refbin
+        sample = (f"{n} bond updates ({n / 3:.2f} Trotter steps, {dt:.1f} s) of the reference itself "
+                  f"(proj/src compiled in place on the Eigen-3.4-subset shim over OpenBLAS LAPACK, "
+                  f"oracle/_ref/ref_bench) in tebd_step order on the same synthetic state, {cores} threads; "
+                  "steps/s = updates/3 / time")
+        kind = "reference"
+    else:
+        warm = 1 if (args.warmup > 0 and chi <= 256) else 0
+        rate, n, dt = cpu_reference_rate(cfg, budget_s=budget if chi > 256 else 0.0,
+                                         min_updates=3 * max(1, args.steps) if chi <= 256 else 1, warmup_updates=warm)
+        sample = (f"{n} bond updates ({n / 3:.2f} Trotter steps, {dt:.1f} s) of the NumPy/LAPACK oracle port in "
+                  f"Trotter order on the same synthetic state and gates (OpenBLAS, {cores} threads); steps/s = "
+                  "updates/3 / time")
+        kind = "port"
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / rate, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
         "config": config_dict(cfg, 1),
-        "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} bond updates ({n / 3:.2f} Trotter steps, {dt:.1f} s) of the NumPy/LAPACK "
-                                   f"oracle port in Trotter order on the same synthetic state and gates "
-                                   f"(OpenBLAS, {cores} threads); steps/s = updates/3 / time",
+        "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": cores, "kind": kind, "sample": sample,
                          "host": host_info()},
         "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
