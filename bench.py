@@ -293,9 +293,9 @@ def reference_binary_rate(cfg, budget_s, min_updates=1, scheme=None):
         with open(path, "wb") as f:
             for a in sites + bonds:
                 f.write(np.ascontiguousarray(a, dtype=np.complex128).tobytes())
-        # OMP_WAIT_POLICY=PASSIVE: the reference's OpenMP phi loop and the BLAS pthreads
-        # pool share the cores (Eigen uses one OpenMP pool for both)
-        env = dict(os.environ, OMP_NUM_THREADS=str(cores), OPENBLAS_NUM_THREADS=str(cores), OMP_WAIT_POLICY="PASSIVE")
+        # the reference is built without OpenMP (oracle/Makefile): its products
+        # run on the OpenBLAS pool, all host cores
+        env = dict(os.environ, OPENBLAS_NUM_THREADS=str(cores))
         out = subprocess.run([REF_BENCH, path, str(d), str(chi), scheme or cfg_scheme, "1" if explicit else "0",
                               str(dabs), str(drel), str(budget_s), str(min_updates)], capture_output=True, text=True,
                              env=env)
