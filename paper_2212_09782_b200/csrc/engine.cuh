@@ -46,7 +46,6 @@ enum Slot : int {
   S_QR_V2,       // reflectors / T factors of the second QR of a pipelined pair
   S_QR_T2,
   S_GEMM_PART3,  // split-K scratch of GEMMs on side4 (consumers of the pair's Q blocks)
-  S_PY0,         // phiev Y0^H of the re-associated X = Xi (phiev Y0^H)
   S_QR_WS,       // W / W2 of the QR look-ahead's wide updates on e.side (GEMM path)
   S_QR_WS2,
   S_GEMM_PARTS,  // split-K scratch of GEMMs on e.side
@@ -165,15 +164,12 @@ bool qr_pair_fits(long long m, long long nc);
 // ldq) from the reflectors the pair left in S_QR_V / S_QR_T, on stream st
 // (left_iso of apply_gate_qr, proj/src/gates.cpp:373)
 void pair_form_q(Engine& e, const double2* x, long long m, long long k, double2* q, long long ldq, cudaStream_t st);
-// on_qblock (optional): called on the Q stream once columns [c0, c0 + nb) of
-// qy are formed and gauge-fixed (consumers of Q start behind the Y chain).
 // Callers may leave work in flight on e.side (the X look-ahead stream: X's
 // columns past the first two panels, first touched there by the wide update)
 // and have e.side2 wait for anything that still reads C (C is first written
 // on e.side2).
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
                        double2* qy, double2* ry,
-                       const std::function<void(long long, long long, cudaStream_t)>& extract,
-                       const std::function<void(long long, long long, cudaStream_t)>& on_qblock = nullptr);
+                       const std::function<void(long long, long long, cudaStream_t)>& extract);
 
 }  // namespace qt

@@ -317,7 +317,7 @@ void qtheta_resid(Engine& e, const double2* qt, long long rows, long long cols, 
 }
 
 void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
-                 const double2* u, int out_scalar, bool phiev_only) {
+                 const double2* u, int out_scalar) {
   const long long d = D.d, cl = D.chi_l, cm = D.chi_m, cn = D.chi_n, cr = D.chi_r;
   const long long blk = cm * d * d * cr;
   double2* phi = e.cbuf(S_PHI, blk);
@@ -343,7 +343,6 @@ void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm,
     g.C = phiev; g.ldc = cr; g.strideC = d * d * cr;
     zgemm(g, gs, e.stream);
   }
-  if (phiev_only) return;
   // theta = Xi (cl x cm) . phiev (cm x d*d*cr)
   gemm(e, Op::N, Op::N, cl, d * d * cr, cm, xi, cm, phiev, d * d * cr, theta, d * d * cr);
   norm2(e, theta, cl * d, d * cr, d * cr, e.dscal + out_scalar);  // (alpha i) x (j delta) view: more rows
@@ -372,14 +371,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   zero_flag_kernel<<<1, 1, 0, e.stream>>>(flag);
   const int sweeps = std::max(1, static_cast<int>(pol.qr_sweeps));
   const bool qtheta = use_qtheta(e, pol, rows);
-  // QT_X_REASSOC=1 (pipelined pair with Y0 = B^n): X = Xi (phiev Y0^H) on the
-  // main stream while theta = Xi phiev is formed on the theta stream (first
-  // needed by the reflector of X's first panel); ||theta|| = ||Q_full^H theta||
-  // afterwards.  Measured no faster at C2 (194 vs 196 steps/s: the theta GEMM
-  // shares the SMs with X and the first panel), so off by default
-  static const bool reassoc = std::getenv("QT_X_REASSOC") != nullptr;
   const bool pair = qtheta && use_qr_pair(rows, cols);
-  const bool x_reassoc = reassoc && pair && eta == cn && sweeps == 1;
   // Y0 = B^n regrouped (gates.cpp:357-361) on e.side while theta is built
   const bool y0_early = (eta == cn) && e.side != nullptr;
   if (y0_early) {
@@ -391,7 +383,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     permute(e, bn, 3, shp, perm, false, y, 1.0, nullptr, e.side);
     QT_CUDA(cudaEventRecord(e.event(1003), e.side));
   }
-  build_theta(e, D, xi, bm, bn, u, SC_THETA2, x_reassoc);
+  build_theta(e, D, xi, bm, bn, u, SC_THETA2);
   ustamp("theta");
   double2* phiev = e.cbuf(S_PHIEV, cm * d * d * cr);
   double2* theta = e.cbuf(S_THETA, cl * d * d * cr);
@@ -422,29 +414,11 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   // ends Q_full^H theta = [Y; Z] is ready -- no explicit Q_m (unless left_iso
   // is wanted), no theta^H Q_m GEMM, and the explicit error needs only
   // ||Y - L Q_n||^2 + ||Z||^2 instead of a theta-sized residual product
-  bool hastings_done = false;
   bool left_pending = false;  // left_iso formed on side4 (pair path), joined at the end
-  if (x_reassoc) {
-    // theta on the theta stream (side2), behind phiev
-    QT_CUDA(cudaEventRecord(e.event(0), e.stream));
-    QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(0), 0));
-    GemmDesc gt;
-    gt.M = cl; gt.N = d * d * cr; gt.K = cm;
-    gt.A = xi; gt.lda = cm;
-    gt.B = phiev; gt.ldb = d * d * cr;
-    gt.C = theta; gt.ldc = d * d * cr;
-    zgemm(gt, e.gemm_scratch2(), e.side2);
-    // P = phiev Y0^H ((cm d) x eta), X = Xi P viewed as (cm) x (d eta) -> (cl d) x eta
-    double2* P = e.cbuf(S_PY0, cm * d * eta);
-    gemm(e, Op::N, Op::H, cm * d, eta, cols, phiev, cols, y0, cols, P, eta);
-    gemm(e, Op::N, Op::N, cl, d * eta, cm, xi, cm, P, d * eta, X, d * eta);
-  }
-  const bool x_split = pair && !x_reassoc && x_split_applies(e, eta);
+  const bool x_split = pair && x_split_applies(e, eta);
   for (int it = 0; it < sweeps; ++it) {
     const double2* xb = it == 0 ? y0 : Qp;  // X = theta xb^H (it = 0) / theta xb (Y0 = Q_n = Qp^H)
-    if (it == 0 && x_reassoc) {
-      // X formed above
-    } else if (x_split) {
+    if (x_split) {
       x_gemm_split(e, rows, eta, cols, theta, xb, it == 0, X, flag);
     } else {
       if (it == 0)
@@ -456,43 +430,10 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     ustamp("X");
     if (pair) {
       // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
-      // QT_QB_HASTINGS=1: the Hastings columns of B~m follow the Q blocks of
-      // Y^H (column block b of B~m = phiev Qp[:, b] as soon as that block of Qp
-      // exists); measured slower at C2 (172 vs 181 steps/s: the per-block
-      // GEMMs contend with both panel chains), so off by default
-      //
-      // QT_HASTINGS_SPLIT=1: two Hastings GEMMs -- the columns of every Q
-      // block but the last, issued on the Q stream once the next-to-last block
-      // exists (overlapping the last Y panel and the last Q block), and the
-      // last block's columns after it; measured 192 vs 194.5 steps/s at C2
-      // (the GEMM delays the last panel), so off by default
-      const GemmScratch gs3 = e.gemm_scratch3();
-      std::function<void(long long, long long, cudaStream_t)> hastings_block;
-      static const bool qb_hastings = std::getenv("QT_QB_HASTINGS") != nullptr;
-      static const bool split_hastings =
-          std::getenv("QT_HASTINGS_SPLIT") && std::atoi(std::getenv("QT_HASTINGS_SPLIT")) != 0;
-      const long long npan_y = ceil_div(eta, 32);
-      auto hastings_cols = [&, gs3](long long c0, long long nb, cudaStream_t st) {
-        GemmDesc g;
-        g.M = cm * d; g.N = nb; g.K = cols;
-        g.A = phiev; g.lda = cols;
-        g.B = Qp + c0; g.ldb = eta;
-        g.C = out.b_m + c0; g.ldc = cm * eta; g.rsplit = d; g.ldc_hi = eta;
-        zgemm(g, gs3, st);
-      };
-      if (out.b_m && qb_hastings)
-        hastings_block = hastings_cols;
-      else if (out.b_m && split_hastings && npan_y >= 3)
-        hastings_block = [&, hastings_cols](long long c0, long long nb, cudaStream_t st) {
-          const long long b = c0 / 32;
-          if (b == npan_y - 2) hastings_cols(0, c0 + nb, st);  // blocks 0 .. npan-2
-          else if (b == npan_y - 1) hastings_cols(c0, nb, st);  // the last block
-        };
-      qr_pair_pipelined(
-          e, X, rows, eta, theta, cols, YH, Qp, Rp,
-          [&](long long r0, long long nr, cudaStream_t st) { qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st); },
-          hastings_block);
-      hastings_done = static_cast<bool>(hastings_block);
+      qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp,
+                        [&](long long r0, long long nr, cudaStream_t st) {
+                          qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st);
+                        });
       if (out.left_iso) {
         // left_iso = Q_m (gates.cpp:373) from X's stored reflectors, on side4
         // concurrently with the tail (Hastings on the main stream)
@@ -506,7 +447,6 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
         left_pending = true;
       }
       check_finite(e, theta, eta * cols, flag);  // Y (the first eta rows of Q_full^H theta)
-      if (x_reassoc) norm2(e, theta, rows, cols, cols, e.dscal + SC_THETA2);  // ||Q_full^H theta|| = ||theta||
       ustamp("pair");
       continue;
     }
@@ -534,8 +474,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   // pair path: the output permutes and the explicit-error products run on
   // e.side, concurrently with the Hastings product on the main stream (they
   // only read L, Q_n and Q_full^H theta; joined before returning)
-  static const bool resid_side = std::getenv("QT_RESID_MAIN") == nullptr;
-  const bool fork_tail = qtheta && resid_side && e.side != nullptr;
+  const bool fork_tail = qtheta && e.side != nullptr;
   const cudaStream_t tail_st = fork_tail ? e.side : e.stream;
   if (fork_tail) {
     QT_CUDA(cudaEventRecord(e.event(1000), e.stream));
@@ -566,7 +505,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     qtheta_resid(e, theta, rows, cols, X, eta, W, e.dscal + SC_RESID, e.side);
     QT_CUDA(cudaEventRecord(e.event(1001), e.side));
   }
-  if (out.b_m && !hastings_done) {
+  if (out.b_m) {
     // B~m[i,beta,k] = sum_{j,delta} phiev[beta,i,j,delta] conj(B~n[j,k,delta])
     //             = (phiev (cm*d x d*cr) . Qp)[(beta i), k]   (gates.cpp:186-190)
     // (skipped when the caller keeps left_iso instead: the reference finite

@@ -40,9 +40,8 @@ struct HostReport {
 // theta build (K1a/K1b/K1c, proj/src/gates.cpp:123-182): fills the engine
 // slots S_PHIEV (beta,i,j,delta) and S_THETA (alpha,i,j,delta); ||theta||^2 is
 // written to dscal[out_scalar].
-// (phiev_only: stop after phiev, theta and its norm are left to the caller)
 void build_theta(Engine& e, const Dims& D, const double2* xi, const double2* bm, const double2* bn,
-                 const double2* u, int out_scalar, bool phiev_only = false);
+                 const double2* u, int out_scalar);
 
 // apply_gate_qr (proj/src/gates.cpp:343-386) with outputs written into
 // caller-allocated buffers sized for eta = qr_eta(policy, D).  Fully

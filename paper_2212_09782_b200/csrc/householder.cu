@@ -66,12 +66,6 @@ struct PanelArgs {
   double2* diag;   // [2][32] broadcast of the current diagonal row
   unsigned* bar;   // grid barrier words
   long long* dbg;  // optional per-column clock64 stamps (CTA 0, thread 0)
-  // fused look-ahead (cluster panel, pre != 0): before factoring, apply the
-  // previous panel's block reflector H_{p-1}^H to this panel's columns -- the
-  // panel rows and the 32 rows above them (R12, A12 = A - 32 lda)
-  const double2* vprev = nullptr;  // V_{p-1} at its own top row (32 rows above A), ld ldv
-  const double2* tprev = nullptr;  // T_{p-1} (32 x 32)
-  int pre = 0;
 };
 
 __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_kernel(PanelArgs a) {
@@ -276,21 +270,13 @@ int grid_for(long long total) {
 template <int RPW>
 void launch_panel_rpw(Engine& e, const PanelArgs& a, long long cs, cudaStream_t st) {
   auto kern = panel_cluster_kernel<RPW>;
-  // the fused look-ahead stages (32 + rows) x 32 V and A tiles: RPW <= 5 (smem)
-  constexpr size_t pre_smem = [] {
-    size_t mx = 0;  // the reduce-scatter inbox depends on the cluster size: max over 1..16
-    for (int c = 1; c <= 16; ++c) mx = panel_pre_smem<RPW>(c) > mx ? panel_pre_smem<RPW>(c) : mx;
-    return RPW <= 5 ? mx : size_t(0);
-  }();
-  constexpr size_t smem_attr = pre_smem > panel_cluster_smem(RPW) ? pre_smem : panel_cluster_smem(RPW);
+  constexpr size_t smem_attr = panel_cluster_smem(RPW);
   static std::once_flag attr_once;
   std::call_once(attr_once, [&] {
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     QT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_attr)));
   });
-  if (a.pre && RPW > 5) throw Error(Err::internal, "fused panel look-ahead needs <= 5 rows per warp");
-  const size_t smem = a.pre ? std::max(panel_cluster_smem(RPW), panel_pre_smem<RPW>(static_cast<int>(cs)))
-                            : panel_cluster_smem(RPW);
+  const size_t smem = panel_cluster_smem(RPW);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(cs));
   cfg.blockDim = dim3(CL_THREADS);
@@ -406,150 +392,9 @@ void launch_panel(Engine& e, const PanelArgs& base, long long mp, cudaStream_t s
   QT_LAUNCHED();
 }
 
-// C <- H_p^H C for a WIDE C (the theta side of the QR pair), split by
-// columns: CTA b owns columns [b*CB, b*CB + CB) over all mp rows, so no
-// cross-CTA reduction is needed.  Pass 1 streams V (mp x 32) and the C block
-// through shared memory in double-buffered 128-row chunks and forms
-// W = V^H C_blk on the FP64 tensor pipe; W2 = T^H W; pass 2 re-streams the
-// chunks and writes C_blk -= V W2.  With yh != nullptr the first nbp rows of
-// the result (final rows of Q_full^H theta) are also written, gauge-phased
-// and conjugate-transposed, as the matching block of Y^H (the extraction).
-constexpr int AC_CB = 16;    // columns per CTA
-constexpr int AC_RC = 128;   // rows per chunk
-constexpr int AC_THREADS = 256;
-
-__global__ void __launch_bounds__(AC_THREADS, 1)
-    apply_cols_kernel(const double2* __restrict__ V, long long ldv, const double2* __restrict__ T, int nbp,
-                      double2* C, long long ldc, long long mp, long long nc, const double2* __restrict__ xa,
-                      long long lda, double2* yh, long long ldy) {
-  extern __shared__ __align__(16) double2 acs[];
-  double2* Vb[2] = {acs, acs + AC_RC * NB};                                  // [RC][32] swizzled
-  double2* Cb[2] = {acs + 2 * AC_RC * NB, acs + 2 * AC_RC * NB + AC_RC * AC_CB};  // [RC][CB] swizzled
-  double2* Ws = acs + 2 * AC_RC * NB + 2 * AC_RC * AC_CB;                    // [32][CB]
-  double2* Tp = Ws + NB * AC_CB;                                             // [32][32] T^H
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const long long c0 = static_cast<long long>(blockIdx.x) * AC_CB;
-  const int ncl = static_cast<int>(min(static_cast<long long>(AC_CB), nc - c0));
-  const int nchunk = static_cast<int>((mp + AC_RC - 1) / AC_RC);
-  auto stage = [&](int ch, int buf) {
-    const long long r0 = static_cast<long long>(ch) * AC_RC;
-    for (int e = tid; e < AC_RC * NB; e += AC_THREADS) {
-      const int r = e / NB, c = e % NB;
-      const bool ok = r0 + r < mp;
-      lb_cp16(&Vb[buf][r * NB + lb_sw(r, c)], ok ? &V[(r0 + r) * ldv + c] : V, ok);
-    }
-    for (int e = tid; e < AC_RC * AC_CB; e += AC_THREADS) {
-      const int r = e / AC_CB, c = e % AC_CB;
-      const bool ok = r0 + r < mp && c < ncl;
-      lb_cp16(&Cb[buf][r * AC_CB + lb_sw(r, c)], ok ? &C[(r0 + r) * ldc + c0 + c] : C, ok);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  for (int e = tid; e < NB * NB; e += AC_THREADS) {
-    const int i = e / NB, k = e % NB;
-    Tp[e] = (i < nbp && k < nbp) ? cconj(T[k * NB + i]) : make_double2(0.0, 0.0);
-  }
-  // ---- pass 1: W = V^H C_blk; warp w owns the 8 x 8 block (w / 2, w % 2)
-  const int ib = w >> 1, cb = w & 1;
-  double cre[2] = {0.0, 0.0}, cim[2] = {0.0, 0.0};
-  stage(0, 0);
-  for (int ch = 0; ch < nchunk; ++ch) {
-    const int buf = ch & 1;
-    if (ch + 1 < nchunk) {
-      stage(ch + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < AC_RC; r += 4) {
-      const int rr = r + t;
-      cmma(cre, cim, cconj(Vb[buf][rr * NB + lb_sw(rr, ib * 8 + g)]), Cb[buf][rr * AC_CB + lb_sw(rr, cb * 8 + g)]);
-    }
-    __syncthreads();  // buffer free for the chunk after next
-  }
-#pragma unroll
-  for (int e2 = 0; e2 < 2; ++e2) Ws[(ib * 8 + g) * AC_CB + cb * 8 + 2 * t + e2] = make_double2(cre[e2], cim[e2]);
-  __syncthreads();
-  // ---- W2 = T^H W (same block ownership), kept in registers as B fragments later
-  {
-    double xre[2] = {0.0, 0.0}, xim[2] = {0.0, 0.0};
-#pragma unroll
-    for (int k0 = 0; k0 < NB; k0 += 4)
-      cmma(xre, xim, Tp[(ib * 8 + g) * NB + k0 + t], Ws[(k0 + t) * AC_CB + cb * 8 + g]);
-    __syncthreads();
-#pragma unroll
-    for (int e2 = 0; e2 < 2; ++e2) Ws[(ib * 8 + g) * AC_CB + cb * 8 + 2 * t + e2] = make_double2(xre[e2], xim[e2]);
-  }
-  __syncthreads();
-  // ---- pass 2: C_blk -= V W2, chunk by chunk (16 x 2 blocks of 8 x 8 per chunk)
-  stage(0, 0);
-  for (int ch = 0; ch < nchunk; ++ch) {
-    const int buf = ch & 1;
-    if (ch + 1 < nchunk) {
-      stage(ch + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const long long r0 = static_cast<long long>(ch) * AC_RC;
-    for (int blk = w; blk < (AC_RC / 8) * (AC_CB / 8); blk += AC_THREADS / 32) {
-      const int rb = blk / (AC_CB / 8), bcb = blk % (AC_CB / 8), row = rb * 8 + g;
-      double ure[2], uim[2];
-#pragma unroll
-      for (int e2 = 0; e2 < 2; ++e2) {
-        const double2 c = Cb[buf][row * AC_CB + lb_sw(row, bcb * 8 + 2 * t + e2)];
-        ure[e2] = c.x;
-        uim[e2] = c.y;
-      }
-#pragma unroll
-      for (int k0 = 0; k0 < NB; k0 += 4) {
-        const double2 av = Vb[buf][row * NB + lb_sw(row, k0 + t)];
-        cmma(ure, uim, make_double2(-av.x, -av.y), Ws[(k0 + t) * AC_CB + bcb * 8 + g]);
-      }
-      const long long gr = r0 + row;
-      if (gr < mp)
-#pragma unroll
-        for (int e2 = 0; e2 < 2; ++e2) {
-          const int col = bcb * 8 + 2 * t + e2;
-          if (col < ncl) {
-            const double2 v = make_double2(ure[e2], uim[e2]);
-            C[gr * ldc + c0 + col] = v;
-            if (yh && gr < nbp) {  // extraction: yh[c, i] = ph_i conj(v), ph_i = R_ii / |R_ii|
-              const double2 dg = xa[gr * lda + gr];
-              const double ad = hypot(dg.x, dg.y);
-              const double2 ph = ad == 0.0 ? make_double2(1.0, 0.0) : make_double2(dg.x / ad, dg.y / ad);
-              yh[(c0 + col) * ldy + gr] = cmul(ph, cconj(v));
-            }
-          }
-        }
-    }
-    __syncthreads();
-  }
-}
-
-constexpr size_t apply_cols_smem() {
-  return (size_t(2) * AC_RC * NB + size_t(2) * AC_RC * AC_CB + NB * AC_CB + NB * NB) * sizeof(double2);
-}
-
-void apply_cols(const double2* Vp, long long ldv, const double2* Tp, int nbp, double2* C, long long ldc, long long mp,
-                long long nc, const double2* xa, long long lda, double2* yh, long long ldy, cudaStream_t st) {
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    QT_CUDA(cudaFuncSetAttribute(apply_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(apply_cols_smem())));
-  });
-  apply_cols_kernel<<<static_cast<unsigned>(ceil_div(nc, AC_CB)), AC_THREADS, apply_cols_smem(), st>>>(
-      Vp, ldv, Tp, nbp, C, ldc, mp, nc, xa, lda, yh, ldy);
-  QT_LAUNCHED();
-}
-
-// C <- H_p^H C = C - V T^H (V^H C) on stream st (three DMMA GEMMs; W/W2 and the
-// split-K scratch belong to that stream)
 // C <- (I - V T' V^H) C for a block of nbp reflectors, T' = T^H (Q^H C, the
-// factorization) or T (Q C, Q formation); T has leading dimension ldt
+// factorization) or T (Q C, Q formation); T has leading dimension ldt; three
+// DMMA GEMMs on stream st (W/W2 and the split-K scratch belong to that stream)
 void apply_block_reflector(const double2* Vp, long long ldv, const double2* Tp, double2* C, long long ldc,
                            long long mp, long long nc, int nbp, double2* W, double2* W2, const GemmScratch& gs,
                            cudaStream_t st, const std::function<void()>& after_top = nullptr, long long ldt = NB,
@@ -808,30 +653,14 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
   if (dbg_on && !dbg_buf) QT_CUDA(cudaMalloc(&dbg_buf, 8 * NB * sizeof(long long)));
   base.dbg = dbg_on ? dbg_buf : nullptr;
 
-  // look-ahead of the trailing update: the next panel's columns on the main
-  // stream, the rest on e.side behind the next panel -- block reflectors in one
-  // cluster launch when m <= 16 x 128, else as three DMMA GEMMs per update
-  // (each stream with its own W buffers and split-K scratch);
-  // QT_QR_NO_LOOKAHEAD disables it
+  // look-ahead of the trailing update (m <= 16 x 128: block reflectors in one
+  // cluster launch): the next panel's columns on the main stream, the rest on
+  // e.side behind the next panel; taller panels take qr_inplace_outer (or,
+  // with QT_QR_OB=0, sequential three-GEMM updates); QT_QR_NO_LOOKAHEAD
+  // disables it
   static const bool la_env = std::getenv("QT_QR_NO_LOOKAHEAD") == nullptr;
-  // QT_QR_GEMM_LA_MAX=m: the GEMM look-ahead for taller panels up to m rows
-  // (QR 5120 x 1024: 9.63 -> 9.09 ms, but the north-star step moves < 0.5%
-  // and the 8-stream C5 chain loses 4%: off by default)
-  static const long long la_gemm_max = std::getenv("QT_QR_GEMM_LA_MAX")
-                                           ? std::atoll(std::getenv("QT_QR_GEMM_LA_MAX"))
-                                           : 0;
   const bool la_cluster = larfb_cluster_fits(m);
-  const bool lookahead = la_env && npan >= 2 && e.side != nullptr && (la_cluster || m <= la_gemm_max);
-  double2 *SW = nullptr, *SW2 = nullptr;
-  GemmScratch gss;
-  if (lookahead && !la_cluster) {
-    SW = e.cbuf(S_QR_WS, static_cast<size_t>(NB) * n);
-    SW2 = e.cbuf(S_QR_WS2, static_cast<size_t>(NB) * n);
-    gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
-    gss.partial_elems = size_t(1) << 22;
-    gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
-    gss.tile_sums_elems = size_t(1) << 16;
-  }
+  const bool lookahead = la_env && npan >= 2 && e.side != nullptr && la_cluster;
   bool wide_pending = false;
   long long last_wide = -1;
   // QrOpts::capply: panel p's reflector reaches C on side2 once the panel is
@@ -859,11 +688,8 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
     if (capply) {
       QT_CUDA(cudaEventRecord(e.event(cev + p), e.stream));
       QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(cev + p), 0));
-      static const bool cl_apply = std::getenv("QT_QTHETA_CLUSTER") != nullptr;
-      if (!cl_apply || !larfb_cluster(e, pa.V, kp, pa.T, opts.capply + j * opts.ldc, opts.ldc, mp, opts.nc, nbp, true,
-                                      e.side2))
-        apply_block_reflector(pa.V, kp, pa.T, opts.capply + j * opts.ldc, opts.ldc, mp, opts.nc, nbp, CW, CW2, gs2,
-                              e.side2);
+      apply_block_reflector(pa.V, kp, pa.T, opts.capply + j * opts.ldc, opts.ldc, mp, opts.nc, nbp, CW, CW2, gs2,
+                            e.side2);
     }
     if (dbg_on) {
       long long h[8 * NB];
@@ -892,17 +718,10 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
         QT_CUDA(cudaEventRecord(e.event(2 * p), e.stream));  // panel p done: V_p, T_p ready
         QT_CUDA(cudaStreamWaitEvent(e.side, e.event(2 * p), 0));
       }
-      if (la_cluster)
-        larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, nn, nbp, true, e.stream);
-      else
-        apply_block_reflector(pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, nn, nbp, W, W2, gs, e.stream);
+      larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, nn, nbp, true, e.stream);
       wide_pending = ntr > nn;
       if (wide_pending) {
-        if (la_cluster)
-          larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp + nn, lda, mp, ntr - nn, nbp, true, e.side);
-        else
-          apply_block_reflector(pa.V, kp, pa.T, a + j * lda + j + nbp + nn, lda, mp, ntr - nn, nbp, SW, SW2, gss,
-                                e.side);
+        larfb_cluster(e, pa.V, kp, pa.T, a + j * lda + j + nbp + nn, lda, mp, ntr - nn, nbp, true, e.side);
         QT_CUDA(cudaEventRecord(e.event(2 * p + 1), e.side));
         last_wide = p;
       }
@@ -1009,18 +828,11 @@ void pair_form_q(Engine& e, const double2* x, long long m, long long k, double2*
 }
 
 namespace {
-// the cluster panel for mp rows would run with <= 5 rows per warp (fused look-ahead)
-bool panel_pre_fits(long long mp) {
-  static const int cs_cap = std::getenv("QT_PANEL_CS") ? std::atoi(std::getenv("QT_PANEL_CS")) : 16;
-  const long long cs_max = std::max(1, std::min(16, cs_cap));
-  return ceil_div(mp, cs_max * CL_WARPS) <= 5;
-}
 }  // namespace
 
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
                        double2* qy, double2* ry,
-                       const std::function<void(long long, long long, cudaStream_t)>& extract,
-                       const std::function<void(long long, long long, cudaStream_t)>& on_qblock) {
+                       const std::function<void(long long, long long, cudaStream_t)>& extract) {
   if (k == 0) return;
   if (k > m || k > nc || !qr_pair_fits(m, nc)) throw Error(Err::internal, "qr_pair_pipelined: shape not supported");
   const long long npan = ceil_div(k, NB);
@@ -1075,13 +887,6 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
   stamp("start", sx);
   bool wide_pending = false;
   long long last_wide = -1;
-  // QT_FUSED_PANEL=1: the look-ahead block update fused into the next panel
-  // (PanelArgs::pre) instead of a separate narrow block-reflector launch.
-  // Measured no faster at C2 (192 vs 195 steps/s: the in-panel update on the
-  // panel's 16 CTAs costs what the 40-CTA launch did), so off by default
-  static const bool fused_env = std::getenv("QT_FUSED_PANEL") != nullptr;
-  const bool fused = fused_env && panel_pre_fits(m) && panel_pre_fits(nc);
-  std::vector<bool> wide_of(static_cast<size_t>(npan), false);
   for (long long p = 0; p < npan; ++p) {
     const long long j = p * NB;
     const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
@@ -1094,51 +899,21 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     pa.V = Vx + j * kp + p * NB;
     pa.ldv = kp;
     pa.T = Tx + p * NB * NB;
-    if (fused && p > 0) {
-      // block p: H_0..H_{p-2} came with the wide updates, H_{p-1} is fused into the panel
-      if (p >= 2 && wide_of[p - 2]) QT_CUDA(cudaStreamWaitEvent(sx, e.event(2 * (p - 2) + 1), 0));
-      pa.pre = 1;
-      pa.vprev = Vx + (j - NB) * kp + (p - 1) * NB;
-      pa.tprev = Tx + (p - 1) * NB * NB;
-    }
     launch_panel(e, pa, m - j, sx);
     stamp("Xpanel" + std::to_string(p), sx);
     // ---- theta side: C <- H_p^H C, then rows [j, j + nbp) of C are final
     QT_CUDA(cudaEventRecord(e.event(P0 + p), sx));
     QT_CUDA(cudaStreamWaitEvent(sa, e.event(P0 + p), 0));
-    // QT_APPLY_COLS=1: one column-split launch (apply_cols_kernel) applies H_p^H
-    // to C and writes block p of Y^H; measured slower at C2 (194 vs 200
-    // steps/s: 80 CTAs each re-streaming all of V hold 80 SMs for ~90 us and
-    // delay both panel chains), so the three-GEMM application is the default
-    static const bool cols_apply = std::getenv("QT_APPLY_COLS") != nullptr;
-    if (cols_apply) {
-      apply_cols(pa.V, kp, pa.T, nbp, c + j * nc, nc, m - j, nc, x + j * k + j, k, yh + j, k, sa);
+    // rows [j, j + nbp) of H_p^H C are final first: publish them as block p
+    // of Y^H before the rest of C is updated
+    apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa, [&] {
+      extract(j, nbp, sa);
       stamp("extract" + std::to_string(p), sa);
       QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
-    } else {
-      // rows [j, j + nbp) of H_p^H C are final first: publish them as block p
-      // of Y^H before the rest of C is updated
-      apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa, [&] {
-        extract(j, nbp, sa);
-        stamp("extract" + std::to_string(p), sa);
-        QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
-      });
-    }
+    });
     // ---- X trailing update (look-ahead: next panel's columns on sx, the rest on sxw)
     const long long ntr = k - j - nbp;
-    if (fused && ntr > 0) {
-      // next panel's columns: fused into that panel; the rest on sxw
-      const long long nn = std::min<long long>(NB, ntr);
-      if (ntr > nn) {
-        QT_CUDA(cudaEventRecord(e.event(2 * p), sx));
-        QT_CUDA(cudaStreamWaitEvent(sxw, e.event(2 * p), 0));
-        larfb_cluster(e, pa.V, kp, pa.T, x + j * k + j + nbp + nn, k, m - j, ntr - nn, nbp, true, sxw);
-        stamp("Xwide" + std::to_string(p), sxw);
-        QT_CUDA(cudaEventRecord(e.event(2 * p + 1), sxw));
-        wide_of[p] = true;
-        last_wide = p;
-      }
-    } else if (ntr > 0) {
+    if (ntr > 0) {
       const long long nn = std::min<long long>(NB, ntr);
       if (p > 0 && wide_pending) QT_CUDA(cudaStreamWaitEvent(sx, e.event(2 * (p - 1) + 1), 0));
       if (ntr > nn) {
@@ -1170,7 +945,7 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
       QT_CUDA(cudaStreamWaitEvent(sy, e.event(E0 + p), 0));
     }
     stamp("Ystart" + std::to_string(p), sy);
-    if (p >= 1 && !fused) {
+    if (p >= 1) {
       const long long jq = (p - 1) * NB;
       larfb_cluster(e, Vy + jq * kp + (p - 1) * NB, kp, Ty + (p - 1) * NB * NB, yh + jq * k + j, k, nc - jq, nbp, NB,
                     true, sy);
@@ -1183,11 +958,6 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     py.V = Vy + j * kp + p * NB;
     py.ldv = kp;
     py.T = Ty + p * NB * NB;
-    if (fused && p >= 1) {  // H'_{p-1} fused into Y panel p
-      py.pre = 1;
-      py.vprev = Vy + (j - NB) * kp + (p - 1) * NB;
-      py.tprev = Ty + (p - 1) * NB * NB;
-    }
     stamp("Yupdate" + std::to_string(p), sy);
     launch_panel(e, py, nc - j, sy);
     stamp("Ypanel" + std::to_string(p), sy);
@@ -1197,7 +967,6 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
       // gauge-fixed on write-back (the phases of its R' diagonal are final after Y panel p)
       if (!larfb_multi(Vy, kp, Ty, qy + j, k, nc, nbp, static_cast<int>(p + 1), k, sq, true, false, yh, k, j))
         throw Error(Err::internal, "qr_pair_pipelined: Q block does not fit a cluster");
-      if (on_qblock) on_qblock(j, nbp, sq);
       stamp("Qblock" + std::to_string(p), sq);
     }
   }
@@ -1222,7 +991,6 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
   if (!qblocks) {
     gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
     QT_LAUNCHED();
-    if (on_qblock) on_qblock(0, k, sy);
   }
   gauge_r_kernel<<<grid_for(k * k), 256, 0, sy>>>(yh, k, ry, k, k, k);
   QT_LAUNCHED();

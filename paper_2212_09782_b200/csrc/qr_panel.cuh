@@ -125,146 +125,6 @@ __device__ __forceinline__ void bulk_push(uint32_t remote_dst, const void* src, 
       : "memory");
 }
 
-// Fused look-ahead of the cluster panel (PanelArgs::pre): A <- H_{p-1}^H A
-// on this panel's columns before factoring them, where H_{p-1} = I - V T V^H
-// is the previous panel's block reflector.  The affected rows are the panel
-// rows (held in registers, y) and the 32 rows above them (R12; CTA 0 only).
-// One staging pass into shared memory (aliasing the panel's work arrays),
-// W = V^H A on the FP64 tensor pipe, one DSMEM reduce-scatter + all-gather
-// (as larfb_cluster_kernel), W2 = T^H W, A -= V W2; bitwise deterministic.
-// Replaces the separate narrow block-reflector launch between two panels.
-__device__ __forceinline__ int pre_sw(int row, int col) { return col ^ (((row & 1) << 2) | (row & 2)); }
-__device__ __forceinline__ void pre_dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-__device__ __forceinline__ void pre_cmma(double (&cre)[2], double (&cim)[2], double2 a, double2 b) {
-  pre_dmma(cre, a.x, b.x);
-  pre_dmma(cre, -a.y, b.y);
-  pre_dmma(cim, a.x, b.y);
-  pre_dmma(cim, a.y, b.x);
-}
-
-template <int RPW>
-constexpr size_t panel_pre_smem(int cs) {
-  return (size_t(2) * (CL_WARPS * RPW + NB) * NB + 3 * NB * NB + size_t(cs) * ((NB + cs - 1) / cs) * NB) *
-         sizeof(double2);
-}
-
-template <int RPW>
-__device__ void panel_pre_update(const PanelArgs& a, double2 (&y)[RPW], unsigned rank, int CS, int r0, int nloc,
-                                 int nbp, int rows_owned, int my_rows, uint64_t* pre_bars, double2* psm) {
-  constexpr int RPC = CL_WARPS * RPW;
-  constexpr int PR = RPC + NB;  // pre rows: 32 R12 rows (CTA 0) + the local panel rows
-  double2* Vs = psm;                 // [PR][32] swizzled
-  double2* As = Vs + PR * NB;        // [PR][32] swizzled
-  double2* Tp = As + PR * NB;        // [32][32] T^H
-  double2* Wf = Tp + NB * NB;        // [32][32] reduced W
-  double2* W2 = Wf + NB * NB;        // [32][32] T^H W
-  double2* rs = W2 + NB * NB;        // [CS][rows_owned][32] reduce-scatter inbox
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  // stage V rows (R12 rows: CTA 0 only) and the R12 rows of A with 16-byte
-  // asynchronous copies, all in flight at once (zero-filled where absent)
-  for (int e = tid; e < PR * NB; e += CL_THREADS) {
-    const int pr = e / NB, c = e % NB;
-    const bool okv = pr < NB ? rank == 0 : pr - NB < nloc;
-    const double2* src = okv ? a.vprev + static_cast<long long>(pr < NB ? pr : NB + r0 + pr - NB) * a.ldv + c : a.vprev;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                     static_cast<uint32_t>(__cvta_generic_to_shared(&Vs[pr * NB + pre_sw(pr, c)]))),
-                 "l"(src), "r"(okv ? 16 : 0)
-                 : "memory");
-    if (pr < NB) {
-      const bool oka = rank == 0 && c < nbp;
-      const double2* srca = oka ? a.A + static_cast<long long>(pr - NB) * a.lda + c : a.A;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(&As[pr * NB + pre_sw(pr, c)]))),
-                   "l"(srca), "r"(oka ? 16 : 0)
-                   : "memory");
-    }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int e = tid; e < NB * NB; e += CL_THREADS) {
-    const int i = e / NB, kk = e % NB;
-    Tp[e] = cconj(a.tprev[kk * NB + i]);
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < RPW; ++i) {
-    const int pr = NB + w + CL_WARPS * i;
-    As[pr * NB + pre_sw(pr, lane)] = y[i];
-  }
-  __syncthreads();
-  // partial W = V^H A (32 x 32): warp w owns the 8 x 8 output block (w / 4, w % 4)
-  const int rb = w >> 2, cb = w & 3;
-  {
-    double cre[2] = {0.0, 0.0}, cim[2] = {0.0, 0.0};
-#pragma unroll 4
-    for (int r = 0; r < PR; r += 4) {
-      const int rr = r + t;
-      pre_cmma(cre, cim, cconj(Vs[rr * NB + pre_sw(rr, rb * 8 + g)]), As[rr * NB + pre_sw(rr, cb * 8 + g)]);
-    }
-    // reduce-scatter: row i -> CTA i % CS, slot (source rank, i / CS)
-    const int i = rb * 8 + g;
-    const unsigned owner = static_cast<unsigned>(i % CS);
-#pragma unroll
-    for (int e2 = 0; e2 < 2; ++e2) {
-      const int jj = cb * 8 + 2 * t + e2;
-      st_async_push(cl_map(&rs[(static_cast<int>(rank) * rows_owned + i / CS) * NB + jj], owner),
-                    make_double2(cre[e2], cim[e2]), cl_map(&pre_bars[0], owner));
-    }
-  }
-  pmbar_wait(&pre_bars[0], 0);
-  // owned rows: fixed-order sum over the sources, all-gathered into every CTA's Wf
-  for (int e = tid; e < my_rows * NB * CS; e += CL_THREADS) {
-    const int ent = e / CS, dst = e % CS;
-    const int li = ent / NB, jj = ent % NB;
-    const int i = static_cast<int>(rank) + li * CS;
-    double2 sum = make_double2(0.0, 0.0);
-    for (int src = 0; src < CS; ++src) sum = cadd(sum, rs[(src * rows_owned + li) * NB + jj]);
-    st_async_push(cl_map(&Wf[i * NB + jj], static_cast<unsigned>(dst)), sum, cl_map(&pre_bars[1], dst));
-  }
-  pmbar_wait(&pre_bars[1], 0);
-  {  // W2 = T^H W
-    double cre[2] = {0.0, 0.0}, cim[2] = {0.0, 0.0};
-#pragma unroll
-    for (int k0 = 0; k0 < NB; k0 += 4)
-      pre_cmma(cre, cim, Tp[(rb * 8 + g) * NB + k0 + t], Wf[(k0 + t) * NB + cb * 8 + g]);
-#pragma unroll
-    for (int e2 = 0; e2 < 2; ++e2) W2[(rb * 8 + g) * NB + cb * 8 + 2 * t + e2] = make_double2(cre[e2], cim[e2]);
-  }
-  __syncthreads();
-  // A -= V W2 over all pre rows (8 x 8 blocks)
-  for (int blk = w; blk < (PR / 8) * 4; blk += CL_WARPS) {
-    const int brb = blk >> 2, bcb = blk & 3, row = brb * 8 + g;
-    double cre[2], cim[2];
-#pragma unroll
-    for (int e2 = 0; e2 < 2; ++e2) {
-      const double2 c = As[row * NB + pre_sw(row, bcb * 8 + 2 * t + e2)];
-      cre[e2] = c.x;
-      cim[e2] = c.y;
-    }
-#pragma unroll
-    for (int k0 = 0; k0 < NB; k0 += 4) {
-      const double2 av = Vs[row * NB + pre_sw(row, k0 + t)];
-      pre_cmma(cre, cim, make_double2(-av.x, -av.y), W2[(k0 + t) * NB + bcb * 8 + g]);
-    }
-#pragma unroll
-    for (int e2 = 0; e2 < 2; ++e2) As[row * NB + pre_sw(row, bcb * 8 + 2 * t + e2)] = make_double2(cre[e2], cim[e2]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < RPW; ++i) {
-    const int pr = NB + w + CL_WARPS * i;
-    y[i] = (lane < nbp) ? As[pr * NB + pre_sw(pr, lane)] : make_double2(0.0, 0.0);
-  }
-  if (rank == 0)
-    for (int e = tid; e < NB * nbp; e += CL_THREADS) {
-      const int pr = e / nbp, c = e % nbp;
-      a.A[static_cast<long long>(pr - NB) * a.lda + c] = As[pr * NB + pre_sw(pr, c)];
-    }
-  __syncthreads();  // the work arrays alias psm: all reads done before the panel reuses it
-}
 
 // Per column c the critical path is: CTA reduction of the partials (warp 0)
 // -> one bulk DSMEM push per peer CTA -> mbarrier wait -> fixed-order combine
@@ -291,8 +151,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
   double2* taus = Z + NB * NB;               // [32]
   double2* scales = taus + NB;               // [32]       reflector scales (CTA 0)
   Reflector* refl = reinterpret_cast<Reflector*>(scales + NB);   // (3 x double2)
-  __shared__ uint64_t bars[2];      // per-column partial exchange (static: the pre-update aliases psm)
-  __shared__ uint64_t pre_bars[2];  // fused look-ahead: reduce-scatter, all-gather
+  __shared__ uint64_t bars[2];  // per-column partial exchange
 
   const int w = threadIdx.x >> 5, k = threadIdx.x & 31;
   const unsigned rank = cluster_rank();
@@ -303,22 +162,12 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
   constexpr unsigned PUSH = NB * sizeof(double2);  // one 32-lane row of double2
   const unsigned bytes_per_col = static_cast<unsigned>(CS + 1) * PUSH;
 
-  const int pre_rows_owned = (NB + CS - 1) / CS;
-  const int pre_my_rows = (NB - static_cast<int>(rank) + CS - 1) / CS;
   if (threadIdx.x == 0) {
     pmbar_init(&bars[0], 1);
     pmbar_init(&bars[1], 1);
-    if (a.pre) {
-      pmbar_init(&pre_bars[0], 1);
-      pmbar_init(&pre_bars[1], 1);
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     pmbar_arm(&bars[0], bytes_per_col);
     if (nbp > 1) pmbar_arm(&bars[1], bytes_per_col);
-    if (a.pre) {
-      pmbar_arm(&pre_bars[0], static_cast<unsigned>(CS * pre_my_rows * NB * sizeof(double2)));
-      pmbar_arm(&pre_bars[1], static_cast<unsigned>(NB * NB * sizeof(double2)));
-    }
   }
   double2 y[RPW];
 #pragma unroll
@@ -326,12 +175,6 @@ __global__ void __launch_bounds__(CL_THREADS, 1) panel_cluster_kernel(PanelArgs 
     const int lr = w + CL_WARPS * i;
     const int gr = r0 + lr;
     y[i] = (lr < nloc && k < nbp) ? a.A[(static_cast<long long>(gr)) * a.lda + k] : make_double2(0.0, 0.0);
-  }
-  if constexpr (RPW <= 5) {  // (the launcher rejects pre for taller panels: staging smem)
-    if (a.pre) {
-      cluster_sync_all();  // pre-update barriers armed everywhere before any push
-      panel_pre_update<RPW>(a, y, rank, CS, r0, nloc, nbp, pre_rows_owned, pre_my_rows, pre_bars, psm);
-    }
   }
   for (int e = threadIdx.x; e < 2 * 16 * NB; e += CL_THREADS) recv[e] = make_double2(0.0, 0.0);
 #pragma unroll
