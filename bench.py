@@ -506,22 +506,44 @@ def run_chain_reference(args, cc):
 
 
 def gemm_traffic(config):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    GEMM shape of this configuration, from the committed ncu --set full
-    capture summarised in profiles/r01_ncu_full_summary.txt (C2: the
-    1280 x 256 x 1280 projection; north star: 5120 x 1024 x 5120); None when
-    no capture of that shape exists."""
-    row = {"c2": "zgemm_c2.ncu-rep", "north": "zgemm_north.ncu-rep"}.get(config)
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_full_summary.txt")
-    if row is None or not os.path.exists(path):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of the
+    dominant GEMM of this configuration, from the committed ncu --set full
+    captures: north star = the X = theta Y0^H GEMM (5120 x 1024 x 5120,
+    profiles/r02/north_theta_x_raw.csv.gz); C2 = the 1280 x 256 x 1280
+    projection (profiles/r01_ncu_full_summary.txt); None when no capture of
+    that shape exists."""
+    import csv
+    import gzip
+    import io
+    here = os.path.dirname(os.path.abspath(__file__))
+    if config == "north":
+        path = os.path.join(here, "profiles", "r02", "north_theta_x_raw.csv.gz")
+        if not os.path.exists(path):
+            return None
+        rows = list(csv.reader(io.StringIO(gzip.open(path, "rt").read())))
+        hdr, units = rows[0], rows[1]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for vals in rows[2:]:
+            d = dict(zip(hdr, zip(vals, units)))
+            if "zgemm_kernel<0, 1" not in d.get("Kernel Name", ("", ""))[0]:
+                continue
+            try:
+                return sum(float(d[k][0].replace(",", "")) * scale[d[k][1]]
+                           for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            except (KeyError, ValueError):
+                return None
+        return None
+    if config != "c2":
+        return None
+    path = os.path.join(here, "profiles", "r01_ncu_full_summary.txt")
+    if not os.path.exists(path):
         return None
     with open(path) as f:
         lines = f.read().splitlines()
     cols = lines[0].split()
     for ln in lines[1:]:
-        if ln.startswith(row):
+        if ln.startswith("zgemm_c2.ncu-rep"):
             vals = ln.split()
-            # report and kernel name are the leading fields; metrics are the last len(cols)-2
             m = dict(zip(cols[2:], vals[-(len(cols) - 2):]))
             try:
                 return (float(m["dram_read_MB"]) + float(m["dram_write_MB"])) * 1e6
@@ -681,8 +703,9 @@ def main():
         "flops_per_step": f_step,
         "peak_source": "FP64 DMMA microbenchmark (csrc/probe.cu, mma.sync m8n8k4 f64 -> DMMA.8x8x4) measured in "
                        "this run; MEASURED_PEAKS.json has no FP64 figure",
-        "traffic_note": "dram bytes per launch of the dominant GEMM shape from the committed ncu --set full "
-                        "capture (profiles/), null if none",
+        "traffic_note": "dram bytes (read + write) per launch of the dominant GEMM (north star: X = theta "
+                        "Y0^H, 5120 x 1024 x 5120; compulsory A+B+C = 587 MB, so ~2x re-reads of theta at 178 flop/B -- compute-bound) from the committed ncu --set "
+                        "full capture (profiles/r02/), null if none",
         "dominant_kernel": {
             "kernel": "zgemm_kernel (mma.sync m8n8k4 f64 -> DMMA, TMA-staged, mbarrier ring)",
             "achieved": gemm_tf, "frac": gemm_tf / dmma_peak if dmma_peak else None,
