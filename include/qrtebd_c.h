@@ -288,6 +288,9 @@ qt_status qt_check_isometric_finite(const qt_finite* f, double tol, double* righ
 typedef struct qt_chain qt_chain;
 typedef struct qt_loopback qt_loopback;
 qt_status qt_nccl_get_unique_id(uint8_t* id128);
+/* diagnostics: a one-rank NCCL communicator sends `bytes` to itself through a
+ * grouped ncclSend/ncclRecv on `device`; *ok = 1 when the bytes round-trip */
+qt_status qt_nccl_selftest(int device, uint64_t bytes, int* ok);
 qt_status qt_loopback_create(int world, qt_loopback** out);
 qt_status qt_loopback_destroy(qt_loopback* l);
 /* the owned sites [*begin, *end) of rank in world */

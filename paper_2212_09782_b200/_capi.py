@@ -119,6 +119,7 @@ SIGNATURES = {
     "qt_finite_step_observed": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32), PP, C.c_int, C.POINTER(qt_policy),
                                           C.POINTER(qt_bond_report), U64P, P, P]),
     "qt_nccl_get_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "qt_nccl_selftest": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_int)]),
     "qt_loopback_create": (C.c_int, [C.c_int, PP]),
     "qt_loopback_destroy": (C.c_int, [P]),
     "qt_chain_partition": (C.c_int, [C.c_uint64, C.c_int, C.c_int, U64P, U64P]),

@@ -362,6 +362,39 @@ qt_status qt_nccl_get_unique_id(uint8_t* id128) {
   });
 }
 
+qt_status qt_nccl_selftest(int device, uint64_t bytes, int* ok_out) {
+  // one-rank NCCL communicator, a grouped send + recv to itself on a stream,
+  // byte-compared: exercises the runtime-resolved NCCL (dlopen), communicator
+  // setup and the grouped point-to-point path the chain uses, on one GPU
+  return guard_chain([&] {
+    if (!ok_out) throw ChainError(QT_ERR_INPUT, "null argument");
+    cuda_ok(cudaSetDevice(device), "cudaSetDevice");
+    ncclUniqueId id;
+    nccl_ok(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    NcclTransport t;
+    nccl_ok(nccl().comm_init_rank(&t.comm, 1, id, 0), "ncclCommInitRank");
+    cudaStream_t st = nullptr;
+    cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    uint8_t *src = nullptr, *dst = nullptr;
+    cuda_ok(cudaMalloc(&src, bytes), "cudaMalloc");
+    cuda_ok(cudaMalloc(&dst, bytes), "cudaMalloc");
+    std::vector<uint8_t> h(bytes), back(bytes, 0);
+    for (uint64_t i = 0; i < bytes; ++i) h[i] = static_cast<uint8_t>((i * 131 + 7) & 0xff);
+    cuda_ok(cudaMemcpy(src, h.data(), bytes, cudaMemcpyHostToDevice), "h2d");
+    cuda_ok(cudaMemset(dst, 0, bytes), "memset");
+    t.group_start();
+    t.send(src, bytes, 0);
+    t.recv(dst, bytes, 0);
+    t.group_end(st);
+    cuda_ok(cudaStreamSynchronize(st), "sync");
+    cuda_ok(cudaMemcpy(back.data(), dst, bytes, cudaMemcpyDeviceToHost), "d2h");
+    *ok_out = std::memcmp(h.data(), back.data(), bytes) == 0 ? 1 : 0;
+    cudaFree(src);
+    cudaFree(dst);
+    cudaStreamDestroy(st);
+  });
+}
+
 qt_status qt_loopback_create(int world, qt_loopback** out) {
   return guard_chain([&] {
     auto* l = new qt_loopback;

@@ -110,3 +110,21 @@ def test_sharded_chain_bitwise_equals_one_rank(world):
     for c in ctxs:
         c.close()
     lb.close()
+
+
+@pytest.mark.parametrize("torch_first", [True, False])
+def test_nccl_transport_selftest(torch_first):
+    """The chain's NCCL path on one GPU: libnccl resolved at run time (torch's
+    build when torch is loaded), a one-rank communicator, grouped send/recv to
+    itself, bytes round-trip (the multi-rank runs need more GPUs)."""
+    import ctypes as C
+    import subprocess
+    import sys
+    code = ("import ctypes as C\n" + ("import torch\n" if torch_first else "") +
+            "from paper_2212_09782_b200 import _capi\n"
+            "lib = _capi.load(); ok = C.c_int(0)\n"
+            "_capi.check(lib.qt_nccl_selftest(0, 21 * 1024 * 1024, C.byref(ok)))\n"
+            "assert ok.value == 1\n" + ("import torch.distributed\n" if not torch_first else "") + "print('NCCL OK')\n")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=__import__("conftest").ROOT)
+    assert p.returncode == 0 and "NCCL OK" in p.stdout, p.stdout + p.stderr[-3000:]
