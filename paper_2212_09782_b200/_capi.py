@@ -155,6 +155,13 @@ def load():
         raise RuntimeError(
             f"{LIB_NAME} not found at {path}: build it with `make -C paper_2212_09782_b200` "
             "(there is no CPU fallback)")
+    # the sharded chain resolves NCCL at run time: point it at torch's bundled
+    # build (if any) so that a later `import torch` finds the same library
+    if "QRTEBD_NCCL_LIB" not in os.environ:
+        import sysconfig
+        cand = Path(sysconfig.get_paths()["purelib"]) / "nvidia" / "nccl" / "lib" / "libnccl.so.2"
+        if cand.exists():
+            os.environ["QRTEBD_NCCL_LIB"] = str(cand)
     lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -73,7 +74,13 @@ struct Nccl {
 const Nccl& nccl() {
   static const Nccl n = [] {
     Nccl x;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // 1. an NCCL already in the process (torch's), 2. QRTEBD_NCCL_LIB (the
+    // Python binding points it at torch's bundled build, so that a later
+    // `import torch` finds the same soname satisfied), 3. the system library
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    const char* env = std::getenv("QRTEBD_NCCL_LIB");
+    if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) throw ChainError(QT_ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
     auto sym = [&](const char* name) {
       void* p = dlsym(h, name);
