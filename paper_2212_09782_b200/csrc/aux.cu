@@ -340,9 +340,9 @@ void norm2(Engine& e, const double2* x, long long rows, long long cols, long lon
 }
 
 void copy2d(Engine& e, const double2* src, long long lds, double2* dst, long long ldd, long long rows,
-            long long cols) {
+            long long cols, cudaStream_t st) {
   if (rows * cols == 0) return;
-  copy2d_kernel<<<grid_for(rows * cols), 256, 0, e.stream>>>(src, lds, dst, ldd, rows, cols);
+  copy2d_kernel<<<grid_for(rows * cols), 256, 0, st ? st : e.stream>>>(src, lds, dst, ldd, rows, cols);
   QT_LAUNCHED();
 }
 

@@ -54,6 +54,13 @@ enum Slot : int {
   S_QR_TOB,      // combined T factors of the outer (multi-panel) blocks of a tall QR
   S_QR_GRAM,     // V_ob^H V_ob of one outer block, and the Z scratch of the T combination
   S_QN,          // Q_n = Qp^H (eta x cols): the Hastings GEMM's B operand read K-major
+  S_QR_TOB2,     // the tall pair's Y^H chain: combined T per outer block,
+  S_QR_GRAM2,    //   Gram / Z scratch,
+  S_QR_YW,       //   W / W2 of its block reflectors,
+  S_QR_YW2,
+  S_QR_TALL,     //   T of all finished Y^H blocks (k x k, left-looking updates),
+  S_QR_TALLZ,    //   the V^H V / Z scratch of its growth,
+  S_QR_PART2,    //   panel scratch
   S_COUNT
 };
 
@@ -123,7 +130,7 @@ void permute(Engine& e, const double2* in, int rank, const long long* shape, con
 void norm2(Engine& e, const double2* x, long long rows, long long cols, long long ld, double* out);
 // dst = src over rows x cols blocks with leading dimensions
 void copy2d(Engine& e, const double2* src, long long lds, double2* dst, long long ldd, long long rows,
-            long long cols);
+            long long cols, cudaStream_t st = nullptr);
 void set_identity(Engine& e, double2* q, long long rows, long long cols, long long ld, cudaStream_t st = nullptr);
 void check_finite(Engine& e, const double2* x, long long n, int* dflag);
 // the same over a (rows x cols, ld) block, on `st` (nullptr: e.stream)
@@ -160,6 +167,17 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 // heights within one block-reflector cluster (qr_pair_fits).  Everything is
 // joined into e.stream on return.
 bool qr_pair_fits(long long m, long long nc);
+// The same sweep for tall blocks (m, nc > 2048, both panels within one
+// cluster): two-level QR(X) with each outer block applied to C (= theta) on
+// e.side2 and its rows of Q_full^H C published through `extract` as columns of
+// Y^H; QR(Y^H) runs on e.side3 one outer block behind, each block first
+// receiving the combined reflector of the finished Y^H blocks (left-looking,
+// one K = J GEMM triple).  Forms Q (nc x k) and R (k x k) of Y^H gauge-fixed,
+// and, with qx != nullptr, X's thin Q (m x k) too.  Joined into e.stream.
+bool qr_pair_tall_fits(long long m, long long nc, long long k);
+void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
+                  double2* qy, double2* ry, double2* qx,
+                  const std::function<void(long long, long long, cudaStream_t)>& extract);
 // After qr_pair_pipelined: the explicit, gauge-fixed thin Q of X (m x k, ld
 // ldq) from the reflectors the pair left in S_QR_V / S_QR_T, on stream st
 // (left_iso of apply_gate_qr, proj/src/gates.cpp:373)

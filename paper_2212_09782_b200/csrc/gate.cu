@@ -450,6 +450,16 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
       ustamp("pair");
       continue;
     }
+    if (qtheta && qr_pair_tall_fits(rows, cols, eta)) {
+      // tall pair: QR(Y^H) one outer block behind QR(X) and the theta application
+      qr_pair_tall(e, X, rows, eta, theta, cols, YH, Qp, Rp, out.left_iso ? Qm : nullptr,
+                   [&](long long r0, long long nr, cudaStream_t st) {
+                     qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st);
+                   });
+      check_finite(e, theta, eta * cols, flag);  // Y
+      ustamp("tall_pair");
+      continue;
+    }
     if (qtheta) {
       QrOpts o;
       o.capply = theta;  // theta <- Q_full^H theta (theta is not read again: ||theta|| is already known)

@@ -463,6 +463,71 @@ int qr_outer_width() {
 
 }  // namespace
 
+namespace {
+// Outer block [J, J + w) of a tall QR: its 32-column panels, each panel's
+// reflector reaching only the rest of the block (narrow GEMMs), on stream st.
+// V's rows [J, J + w) x cols [J, J + w) are zeroed above each panel's own rows
+// first (the panels write their unit-lower triangles and everything below).
+void outer_block_factor(Engine& e, double2* a, long long lda, long long m, long long k, double2* V, long long kp,
+                        double2* T, long long J, long long w, double2* W, double2* W2, const GemmScratch& gs,
+                        const PanelArgs& base, cudaStream_t st) {
+  const int npb = static_cast<int>(ceil_div(w, NB));
+  QT_CUDA(cudaMemset2DAsync(V + J * kp + J, kp * sizeof(double2), 0, w * sizeof(double2), w, st));
+  for (int c = 0; c < npb; ++c) {
+    const long long j = J + static_cast<long long>(c) * NB;
+    const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
+    const long long mp = m - j;
+    PanelArgs pa = base;
+    pa.A = a + j * lda + j;
+    pa.lda = lda;
+    pa.ldv = kp;
+    pa.mp = mp;
+    pa.nbp = nbp;
+    pa.V = V + j * kp + j;
+    pa.T = T + (j / NB) * NB * NB;
+    launch_panel(e, pa, mp, st);
+    const long long ninner = J + w - (j + nbp);
+    if (ninner > 0) apply_block_reflector(pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, ninner, nbp, W, W2, gs, st);
+  }
+}
+
+// T_ob (ld ob) of outer block [J, J + w): the panels' T factors on the
+// diagonal, T_ob[0:c0, c0:c0+32] = -T_prev (V_prev^H V_c) T_c above it
+void outer_block_tob(Engine& e, const double2* V, long long kp, const double2* T, long long J, long long w,
+                     long long k, long long m, double2* Tb, int ob, double2* G, double2* Z, const GemmScratch& gs,
+                     cudaStream_t st) {
+  const int npb = static_cast<int>(ceil_div(w, NB));
+  const double2* Vb = V + J * kp + J;
+  tob_init_kernel<<<static_cast<int>(ceil_div(static_cast<long long>(ob) * ob, 256)), 256, 0, st>>>(T, J, k, npb, Tb,
+                                                                                                      ob);
+  QT_LAUNCHED();
+  if (npb <= 1) return;
+  GemmDesc gg;
+  gg.M = w; gg.N = w; gg.K = m - J;
+  gg.opA = Op::H; gg.A = Vb; gg.lda = kp;
+  gg.opB = Op::N; gg.B = Vb; gg.ldb = kp;
+  gg.C = G; gg.ldc = ob;
+  zgemm(gg, gs, st);
+  for (int c = 1; c < npb; ++c) {
+    const long long c0 = static_cast<long long>(c) * NB;
+    const long long nbc = std::min<long long>(NB, w - c0);
+    GemmDesc gz;  // Z = (V_prev^H V_c) T_c
+    gz.M = c0; gz.N = nbc; gz.K = nbc;
+    gz.A = G + c0; gz.lda = ob;
+    gz.B = T + (J / NB + c) * NB * NB; gz.ldb = NB;
+    gz.C = Z; gz.ldc = NB;
+    zgemm(gz, gs, st);
+    GemmDesc gx;  // T_ob[0:c0, c0:c0+nbc] = -T_prev Z
+    gx.M = c0; gx.N = nbc; gx.K = c0;
+    gx.A = Tb; gx.lda = ob;
+    gx.B = Z; gx.ldb = NB;
+    gx.C = Tb + c0; gx.ldc = ob;
+    gx.alpha = -1.0; gx.beta = 0.0;
+    zgemm(gx, gs, st);
+  }
+}
+}  // namespace
+
 // Tall QR (panels beyond one block-reflector cluster, m > 2048): two-level
 // blocking.  Panels of NB = 32 columns are factored inside outer blocks of OB
 // columns (QT_QR_OB, default 128), each panel's reflector reaching only the
@@ -520,56 +585,10 @@ void qr_inplace_outer(Engine& e, double2* a, long long m, long long n, long long
     const long long w = std::min<long long>(OB, k - J);  // reflectors in this block
     const long long mb = m - J;
     const int npb = static_cast<int>(ceil_div(w, NB));
-    // V's block rows [J, J + w) x cols [J, J + w): zero above each panel's own
-    // rows (the panels write their unit-lower triangles and everything below)
-    QT_CUDA(cudaMemset2DAsync(V + J * kp + J, kp * sizeof(double2), 0, w * sizeof(double2), w, e.stream));
-    for (int c = 0; c < npb; ++c) {
-      const long long j = J + static_cast<long long>(c) * NB;
-      const int nbp = static_cast<int>(std::min<long long>(NB, k - j));
-      const long long mp = m - j;
-      PanelArgs pa = base;
-      pa.A = a + j * lda + j;
-      pa.mp = mp;
-      pa.nbp = nbp;
-      pa.V = V + j * kp + j;
-      pa.T = T + (j / NB) * NB * NB;
-      launch_panel(e, pa, mp);
-      // inner update: the rest of this outer block only
-      const long long ninner = J + w - (j + nbp);
-      if (ninner > 0)
-        apply_block_reflector(pa.V, kp, pa.T, a + j * lda + j + nbp, lda, mp, ninner, nbp, W, W2, gs, e.stream);
-    }
-    // T_ob: Gram of the block's reflectors, then the off-diagonal blocks
+    outer_block_factor(e, a, lda, m, k, V, kp, T, J, w, W, W2, gs, base, e.stream);
     double2* Tb = TOB + b * OB * OB;
     const double2* Vb = V + J * kp + J;
-    tob_init_kernel<<<static_cast<int>(ceil_div(static_cast<long long>(OB) * OB, 256)), 256, 0, e.stream>>>(
-        T, J, k, npb, Tb, OB);
-    QT_LAUNCHED();
-    if (npb > 1) {
-      GemmDesc gg;
-      gg.M = w; gg.N = w; gg.K = mb;
-      gg.opA = Op::H; gg.A = Vb; gg.lda = kp;
-      gg.opB = Op::N; gg.B = Vb; gg.ldb = kp;
-      gg.C = G; gg.ldc = OB;
-      zgemm(gg, gs, e.stream);
-      for (int c = 1; c < npb; ++c) {
-        const long long c0 = static_cast<long long>(c) * NB;
-        const long long nbc = std::min<long long>(NB, w - c0);
-        GemmDesc gz;  // Z = (V_prev^H V_c) T_c
-        gz.M = c0; gz.N = nbc; gz.K = nbc;
-        gz.A = G + c0; gz.lda = OB;
-        gz.B = T + (J / NB + c) * NB * NB; gz.ldb = NB;
-        gz.C = Z; gz.ldc = NB;
-        zgemm(gz, gs, e.stream);
-        GemmDesc gx;  // T_ob[0:c0, c0:c0+nbc] = -T_prev Z
-        gx.M = c0; gx.N = nbc; gx.K = c0;
-        gx.A = Tb; gx.lda = OB;
-        gx.B = Z; gx.ldb = NB;
-        gx.C = Tb + c0; gx.ldc = OB;
-        gx.alpha = -1.0; gx.beta = 0.0;
-        zgemm(gx, gs, e.stream);
-      }
-    }
+    outer_block_tob(e, V, kp, T, J, w, k, m, Tb, OB, G, Z, gs, e.stream);
     if (capply) {  // C <- Q_ob^H C on side2, behind this block
       QT_CUDA(cudaEventRecord(e.event(ev0 + 2 * b), e.stream));
       QT_CUDA(cudaStreamWaitEvent(e.side2, e.event(ev0 + 2 * b), 0));
@@ -616,6 +635,164 @@ void qr_inplace_outer(Engine& e, double2* a, long long m, long long n, long long
     gauge_r_kernel<<<grid_for(k * n), 256, 0, e.stream>>>(a, lda, r, ldr, k, n);
     QT_LAUNCHED();
   }
+}
+
+bool qr_pair_tall_fits(long long m, long long nc, long long k) {
+  static const bool off = std::getenv("QT_NO_TALL_PAIR") != nullptr;
+  // both chains on cluster panels (<= 5120 rows): two grid-barrier panels in
+  // flight at once could each hold part of the GPU while waiting for the rest
+  return !off && qr_outer_width() > 0 && !larfb_cluster_fits(m) && !larfb_cluster_fits(nc) && m <= 5120 &&
+         nc <= 5120 && k > NB && k <= m && k <= nc;
+}
+
+void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
+                  double2* qy, double2* ry, double2* qx,
+                  const std::function<void(long long, long long, cudaStream_t)>& extract) {
+  const int OB = qr_outer_width();
+  const long long npan = ceil_div(k, NB);
+  const long long kp = npan * NB;
+  const long long nob = ceil_div(k, static_cast<long long>(OB));
+  const cudaStream_t sx = e.stream, sxw = e.side, sa = e.side2, sy = e.side3;
+  // X chain (main + look-ahead side stream) and the theta application (side2)
+  double2* V = e.cbuf(S_QR_V, static_cast<size_t>(m) * kp);
+  double2* T = e.cbuf(S_QR_T, static_cast<size_t>(npan) * NB * NB);
+  double2* TOB = e.cbuf(S_QR_TOB, static_cast<size_t>(nob) * OB * OB);
+  double2* G = e.cbuf(S_QR_GRAM, static_cast<size_t>(OB) * OB + static_cast<size_t>(OB) * NB);
+  double2* W = e.cbuf(S_QR_W, static_cast<size_t>(OB) * k);
+  double2* W2 = e.cbuf(S_QR_W2, static_cast<size_t>(OB) * k);
+  double2* SW = e.cbuf(S_QR_WS, static_cast<size_t>(OB) * k);
+  double2* SW2 = e.cbuf(S_QR_WS2, static_cast<size_t>(OB) * k);
+  double2* CW = e.cbuf(S_QA_W, static_cast<size_t>(OB) * nc);
+  double2* CW2 = e.cbuf(S_QA_W2, static_cast<size_t>(OB) * nc);
+  double2* part = e.cbuf(S_QR_PART, static_cast<size_t>(2) * kNumSMs * NB + 2 * NB);
+  // Y^H chain (side3)
+  double2* Vy = e.cbuf(S_QR_V2, static_cast<size_t>(nc) * kp);
+  double2* Ty = e.cbuf(S_QR_T2, static_cast<size_t>(npan) * NB * NB);
+  double2* TOBy = e.cbuf(S_QR_TOB2, static_cast<size_t>(nob) * OB * OB);
+  double2* Gy = e.cbuf(S_QR_GRAM2, static_cast<size_t>(OB) * OB + static_cast<size_t>(OB) * NB);
+  double2* YW = e.cbuf(S_QR_YW, static_cast<size_t>(k) * std::max(nc, k));
+  double2* YW2 = e.cbuf(S_QR_YW2, static_cast<size_t>(k) * std::max(nc, k));
+  double2* TALL = e.cbuf(S_QR_TALL, static_cast<size_t>(k) * k);
+  double2* TZ = e.cbuf(S_QR_TALLZ, static_cast<size_t>(2) * k * OB);
+  double2* party = e.cbuf(S_QR_PART2, static_cast<size_t>(2) * kNumSMs * NB + 2 * NB);
+  const GemmScratch gs = e.gemm_scratch();
+  GemmScratch gss;
+  gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
+  gss.partial_elems = size_t(1) << 22;
+  gss.tile_sums = e.dbuf(S_TILE_SUMSS, size_t(1) << 16);
+  gss.tile_sums_elems = size_t(1) << 16;
+  const GemmScratch gs2 = e.gemm_scratch2(), gsy = e.gemm_scratch3();
+
+  PanelArgs bx{};
+  bx.part = part;
+  bx.diag = part + 2 * kNumSMs * NB;
+  bx.bar = e.barrier;
+  bx.dbg = nullptr;
+  PanelArgs by = bx;
+  by.part = party;
+  by.diag = party + 2 * kNumSMs * NB;
+  by.bar = e.barrier + 16;
+
+  // events: 4000 + 4b: X block b's T ready; +1: X side update done; +2: rows
+  // of Y^H block b published; 4000 + 4 nob: start / joins
+  const size_t ev0 = 4000, evs = ev0 + 4 * static_cast<size_t>(nob);
+  QT_CUDA(cudaEventRecord(e.event(evs), sx));  // everything earlier on sx precedes both side chains
+  QT_CUDA(cudaStreamWaitEvent(sy, e.event(evs), 0));
+  QT_CUDA(cudaStreamWaitEvent(sa, e.event(evs), 0));
+  QT_CUDA(cudaMemsetAsync(TALL, 0, static_cast<size_t>(k) * k * sizeof(double2), sy));
+  // the combined reflector of the finished Y^H blocks is used from row 0: the
+  // rows above each block's own diagonal block must be zero
+  QT_CUDA(cudaMemsetAsync(Vy, 0, static_cast<size_t>(nc) * kp * sizeof(double2), sy));
+  long long side_last = -1;
+  for (long long b = 0; b < nob; ++b) {
+    const long long J = b * OB;
+    const long long w = std::min<long long>(OB, k - J);
+    // ---- X block b (main stream), T_ob
+    outer_block_factor(e, x, k, m, k, V, kp, T, J, w, W, W2, gs, bx, sx);
+    double2* Tb = TOB + b * OB * OB;
+    const double2* Vb = V + J * kp + J;
+    outer_block_tob(e, V, kp, T, J, w, k, m, Tb, OB, G, G + static_cast<size_t>(OB) * OB, gs, sx);
+    QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b), sx));
+    // ---- theta side: C <- Q_ob^H C, then rows [J, J + w) of C are final:
+    // published as columns [J, J + w) of Y^H
+    QT_CUDA(cudaStreamWaitEvent(sa, e.event(ev0 + 4 * b), 0));
+    apply_block_reflector(Vb, kp, Tb, c + J * nc, nc, m - J, nc, static_cast<int>(w), CW, CW2, gs2, sa,
+                          [&] { extract(J, w, sa); }, OB, true);
+    QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b + 2), sa));
+    // ---- X look-ahead: the next block's columns on sx, the rest on sxw
+    const long long ntr = k - (J + w);
+    if (ntr > 0) {
+      const long long nn = std::min<long long>(OB, ntr);
+      if (side_last >= 0) QT_CUDA(cudaStreamWaitEvent(sx, e.event(ev0 + 4 * side_last + 1), 0));
+      if (ntr > nn) QT_CUDA(cudaStreamWaitEvent(sxw, e.event(ev0 + 4 * b), 0));
+      apply_block_reflector(Vb, kp, Tb, x + J * k + J + w, k, m - J, nn, static_cast<int>(w), W, W2, gs, sx, nullptr,
+                            OB, true);
+      if (ntr > nn) {
+        apply_block_reflector(Vb, kp, Tb, x + J * k + J + w + nn, k, m - J, ntr - nn, static_cast<int>(w), SW, SW2,
+                              gss, sxw, nullptr, OB, true);
+        QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b + 1), sxw));
+        side_last = b;
+      }
+    }
+    // ---- Y^H block b (side3): the finished blocks' combined reflector
+    // (left-looking), its panels, its T_ob, and T_all's new block column
+    QT_CUDA(cudaStreamWaitEvent(sy, e.event(ev0 + 4 * b + 2), 0));
+    if (b > 0)
+      apply_block_reflector(Vy, kp, TALL, yh + J, k, nc, w, static_cast<int>(J), YW, YW2, gsy, sy, nullptr, k, true);
+    outer_block_factor(e, yh, k, nc, k, Vy, kp, Ty, J, w, YW, YW2, gsy, by, sy);
+    double2* Tyb = TOBy + b * OB * OB;
+    outer_block_tob(e, Vy, kp, Ty, J, w, k, nc, Tyb, OB, Gy, Gy + static_cast<size_t>(OB) * OB, gsy, sy);
+    copy2d(e, Tyb, OB, TALL + J * k + J, k, w, w, sy);
+    if (b > 0) {
+      GemmDesc gg;  // V_prev^H V_b (J x w), rows J.. of both (V_prev is zero above its own rows < J only)
+      gg.M = J; gg.N = w; gg.K = nc - J;
+      gg.opA = Op::H; gg.A = Vy + J * kp; gg.lda = kp;
+      gg.B = Vy + J * kp + J; gg.ldb = kp;
+      gg.C = TZ; gg.ldc = w;
+      zgemm(gg, gsy, sy);
+      GemmDesc gz;  // Z = (V_prev^H V_b) T_b
+      gz.M = J; gz.N = w; gz.K = w;
+      gz.A = TZ; gz.lda = w;
+      gz.B = Tyb; gz.ldb = OB;
+      gz.C = TZ + J * w; gz.ldc = w;
+      zgemm(gz, gsy, sy);
+      GemmDesc gx;  // T_all[0:J, J:J+w] = -T_all[0:J, 0:J] Z
+      gx.M = J; gx.N = w; gx.K = J;
+      gx.A = TALL; gx.lda = k;
+      gx.B = TZ + J * w; gx.ldb = w;
+      gx.C = TALL + J; gx.ldc = k;
+      gx.alpha = -1.0; gx.beta = 0.0;
+      zgemm(gx, gsy, sy);
+    }
+  }
+  // ---- explicit, gauge-fixed Q and R of Y^H (side3), X's Q if asked (side2)
+  set_identity(e, qy, nc, k, k, sy);
+  for (long long b = nob - 1; b >= 0; --b) {
+    const long long J = b * OB;
+    const long long w = std::min<long long>(OB, k - J);
+    apply_block_reflector(Vy + J * kp + J, kp, TOBy + b * OB * OB, qy + J * k + J, k, nc - J, k - J,
+                          static_cast<int>(w), YW, YW2, gsy, sy, nullptr, OB, false);
+  }
+  gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
+  QT_LAUNCHED();
+  gauge_r_kernel<<<grid_for(k * k), 256, 0, sy>>>(yh, k, ry, k, k, k);
+  QT_LAUNCHED();
+  if (side_last >= 0) QT_CUDA(cudaStreamWaitEvent(sx, e.event(ev0 + 4 * side_last + 1), 0));
+  if (qx) {  // X's Q (left_iso), backward over X's outer blocks on sx after the factorization
+    set_identity(e, qx, m, k, k, sx);
+    for (long long b = nob - 1; b >= 0; --b) {
+      const long long J = b * OB;
+      const long long w = std::min<long long>(OB, k - J);
+      apply_block_reflector(V + J * kp + J, kp, TOB + b * OB * OB, qx + J * k + J, k, m - J, k - J,
+                            static_cast<int>(w), W, W2, gs, sx, nullptr, OB, false);
+    }
+    gauge_q_kernel<<<grid_for(m * k), 256, 0, sx>>>(x, k, qx, k, m, k);
+    QT_LAUNCHED();
+  }
+  QT_CUDA(cudaEventRecord(e.event(evs + 1), sa));
+  QT_CUDA(cudaStreamWaitEvent(sx, e.event(evs + 1), 0));
+  QT_CUDA(cudaEventRecord(e.event(evs + 2), sy));
+  QT_CUDA(cudaStreamWaitEvent(sx, e.event(evs + 2), 0));
 }
 
 namespace {
