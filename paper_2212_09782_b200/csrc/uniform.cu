@@ -314,7 +314,10 @@ std::vector<StepRecord> uniform_step(UniformDev* s, const std::vector<std::pair<
       QT_CUDA(cudaStreamEndCapture(e.stream, &g));
       UniformDev::GraphEntry ge;
       ge.arena_gen = s->arena_gen();
-      QT_CUDA(cudaGraphInstantiate(&ge.exec, g, 0));
+      // keep the captured stream priorities (latency-bound panel chains above
+      // the side streams' GEMMs); by default a graph runs every kernel node at
+      // the launch stream's priority
+      QT_CUDA(cudaGraphInstantiateWithFlags(&ge.exec, g, cudaGraphInstantiateFlagUseNodePriority));
       QT_CUDA(cudaGraphDestroy(g));
       ge.prof = gemm_profile_take_captured();
       // captured launches are not executed: count them at replay instead
