@@ -19,8 +19,9 @@
 //      (Y,X) is written as its conjugate transpose) and every row chunk
 //      V[r,Y] <- V[r,Y] J_Y, as m8n8k4 DMMA products in shared memory.
 // Rounds are separated by a grid barrier on a monotonic arrival counter.
-// Sweeps stop when no rotation in a full sweep met the criterion of make_rot,
-// at most 30 sweeps.  Every reduction has a fixed order: results are bitwise
+// Sweeps stop when, after a sweep, no off-diagonal entry meets the criterion
+// of make_rot (a grid-wide scan: a further sweep would rotate nothing), at
+// most 30 sweeps.  Every reduction has a fixed order: results are bitwise
 // reproducible run to run.
 #include <cstdio>
 #include <cstdlib>
@@ -57,7 +58,7 @@ struct JacobiArgs {
   double2* V;     // N x N
   double2* Jbuf;  // [2 round parities][npairs][JX][JX]
   double* flags;  // [MAX_SWEEPS] per-sweep max |offdiag| (reduced per CTA into slots below)
-  double* cta_max;  // [gridDim][2]
+  double* cta_max;  // [2][gridDim]: per-CTA "an entry still meets the criterion" of the end-of-sweep scan
   unsigned* bar;
   int N, nb;
   int full_inner;  // 1: full inner sweep in every outer round (QT_JACOBI_FULL)
@@ -76,18 +77,6 @@ struct Rot {
   double2 e;  // e^{-i phi}
   bool active;
 };
-
-// 1/x to full precision: hardware approximation + one Newton step (the
-// rotation only needs a few-ulp accurate angle; the latency of IEEE division
-// sits on the inner sweep's critical path)
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 // power-of-two scale bringing ||G||_F into [1, 2): exact, so the eigenvalues
 // are recovered bit-exactly and the squared magnitudes below cannot underflow
@@ -114,12 +103,28 @@ __device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double to
     r.e = make_double2(1.0, 0.0);
     return r;
   }
+  // t = tan = sign(d) 2|c| / (|d| + sqrt(d^2 + 4|c|^2)), d = b - a, written so
+  // that only two transcendental steps are dependent: with s = |d| + sqrt(..),
+  // cs = s / sqrt(s^2 + 4|c|^2) and sn = sign(d) 2|c| / sqrt(s^2 + 4|c|^2);
+  // |c| and the phase come from rsqrt(|c|^2) alongside
+#ifdef QT_JACOBI_OLD_ROT
+  {
+    const double inv_ac = rsqrt(ac2);
+    r.e = make_double2(c.x * inv_ac, -c.y * inv_ac);
+    const double theta = (b - a) * 0.5 * inv_ac;
+    const double t = copysign(1.0 / (fabs(theta) + sqrt(fma(theta, theta, 1.0))), theta);
+    r.cs = rsqrt(fma(t, t, 1.0));
+    r.sn = t * r.cs;
+    return r;
+  }
+#endif
+  const double d = b - a;
   const double inv_ac = rsqrt(ac2);
+  const double s = fabs(d) + sqrt(fma(d, d, 4.0 * ac2));
+  const double inv = rsqrt(fma(s, s, 4.0 * ac2));
   r.e = make_double2(c.x * inv_ac, -c.y * inv_ac);
-  const double theta = (b - a) * 0.5 * inv_ac;  // |theta| <= ~1e22 on the scaled matrix
-  const double t = copysign(rcp_nr(fabs(theta) + sqrt(fma(theta, theta, 1.0))), theta);
-  r.cs = rsqrt(fma(t, t, 1.0));
-  r.sn = t * r.cs;
+  r.cs = s * inv;
+  r.sn = copysign(2.0 * ac2 * inv_ac * inv, d);
   return r;
 }
 
@@ -231,7 +236,6 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   const bool stamp = a.prof && tid == 0 && cta == 0;
   long long pa = 0, pw = 0, pb = 0, ps = 0;
   unsigned epoch = 0;
-  double mx = 0.0;  // any rotation met the criterion in this CTA during the current sweep
 
   // ---- round-robin bookkeeping: block at position j of round r; pair of a
   // block in round r; the block paired with b in round r
@@ -266,15 +270,15 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     // block is paired there); later rounds rotate the cross pairs only --
     // every pair is still rotated once per sweep.  Per inner round: JB
     // threads form the rotations once, then the thread owning the 2x2 block
-    // (k,l) writes U_k^H S_kl U_l and J_kl U_l in place.
+    // (k,l) writes U_k^H S_kl U_l and J_kl U_l in place.  (Forming the
+    // rotations redundantly in every thread to save the first barrier loses:
+    // the FP64 pipe, not the barrier, is the limit.)
     const int n_inner = (round == 0 || a.full_inner) ? JX - 1 : JB;
     for (int ir = 0; ir < n_inner; ++ir) {
       if (tid < JB) {
         int p0, q0;
         inner_pair(tid, ir, JB, p0, q0);
-        const Rot rr = make_rot(S[p0][p0].x, S[q0][q0].x, S[p0][q0], tol2, abs_tol2);
-        if (rr.active) mx = 1.0;
-        rots[tid] = rr;
+        rots[tid] = make_rot(S[p0][p0].x, S[q0][q0].x, S[p0][q0], tol2, abs_tol2);
         rp[tid] = p0;
         rq[tid] = q0;
       }
@@ -375,18 +379,6 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
       } while (v < rg);
     }
   };
-  // CTA-wide "any rotation this sweep" -> cta_max[sweep & 1][cta]; reset
-  auto publish = [&](int sweep) {
-    red[tid] = mx;
-    __syncthreads();
-    for (int w = JT / 2; w > 0; w >>= 1) {
-      if (tid < w) red[tid] = fmax(red[tid], red[tid + w]);
-      __syncthreads();
-    }
-    if (tid == 0) a.cta_max[(sweep & 1) * G + cta] = red[0];
-    mx = 0.0;
-  };
-
   // ---- schedule: phase A of round 0, barrier; then every iteration runs
   // phase B of round (sw, rd) and, overlapped with it, phase A of the next
   // round: the 2P pair tiles the next subproblems read (the diagonal tiles,
@@ -394,24 +386,13 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   // flagged; the CTAs < P wait for their three tiles and solve; the other
   // CTAs finish the remaining tiles; one grid barrier per round.
   if (cta < P) phase_a(0, 0, cta);
-  if (R1 == 1) publish(0);
   jgrid_sync(a.bar, G, epoch);
   int sw = 0, rd = 0;
   bool conv = false;
   for (;;) {
     long long t0 = stamp ? clock64() : 0;
-    bool done = false;
-    if (rd == R1 - 1) {  // every phase A of sweep sw has run: converged if none rotated
-      if (tid == 0) {
-        double m = 0.0;
-        for (int b = 0; b < G; ++b) m = fmax(m, __ldcg(&a.cta_max[(sw & 1) * G + b]));
-        done_flag = m == 0.0;
-      }
-      __syncthreads();
-      done = done_flag != 0;
-    }
     const int ns = rd == R1 - 1 ? sw + 1 : sw, nr = rd == R1 - 1 ? 0 : rd + 1;
-    const bool doA = !done && ns < MAX_SWEEPS;
+    const bool doA = ns < MAX_SWEEPS;
     const long long gcur = static_cast<long long>(sw) * R1 + rd;  // global round index
     const unsigned rg = static_cast<unsigned>(gcur + 1);
     // critical off-diagonal tile of next pair q: the pairs (round rd) of its blocks
@@ -478,14 +459,45 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
         }
       }
     if (stamp) pb += clock64() - t1;
-    if (doA && nr == R1 - 1) publish(ns);
-    if (!doA) {
-      conv = done;
-      sw = ns;
-      break;
-    }
     long long t3 = stamp ? clock64() : 0;
     jgrid_sync(a.bar, G, epoch);
+    if (rd == R1 - 1) {
+      // sweep sw is complete and G holds its result: a further sweep rotates
+      // iff some off-diagonal entry meets make_rot's criterion (the phase A
+      // solves of the next round, run speculatively above, then rotated
+      // nothing).  This scan replaces a whole verification sweep.
+      double any = 0.0;
+      const long long NN = static_cast<long long>(N) * N;
+      for (long long e = static_cast<long long>(cta) * JT + tid; e < NN; e += static_cast<long long>(G) * JT) {
+        const int i = static_cast<int>(e / N), j = static_cast<int>(e % N);
+        if (j <= i) continue;
+        const double2 c = __ldcg(&a.G[e]);
+        const double ac2 = fma(c.x, c.x, c.y * c.y);
+        if (ac2 > abs_tol2 &&
+            ac2 > tol2 * fabs(__ldcg(&a.G[static_cast<long long>(i) * (N + 1)].x) *
+                              __ldcg(&a.G[static_cast<long long>(j) * (N + 1)].x)))
+          any = 1.0;
+      }
+      red[tid] = any;
+      __syncthreads();
+      for (int w = JT / 2; w > 0; w >>= 1) {
+        if (tid < w) red[tid] = fmax(red[tid], red[tid + w]);
+        __syncthreads();
+      }
+      if (tid == 0) a.cta_max[(sw & 1) * G + cta] = red[0];
+      jgrid_sync(a.bar, G, epoch);
+      if (tid == 0) {
+        double m = 0.0;
+        for (int b = 0; b < G; ++b) m = fmax(m, __ldcg(&a.cta_max[(sw & 1) * G + b]));
+        done_flag = m == 0.0;
+      }
+      __syncthreads();
+      if (done_flag || !doA) {
+        conv = done_flag != 0;
+        sw = ns;
+        break;
+      }
+    }
     if (stamp) ps += clock64() - t3 + (t1 - t0);
     sw = ns;
     rd = nr;
