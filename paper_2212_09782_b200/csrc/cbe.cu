@@ -101,10 +101,7 @@ CbeResult gate_cbe(Engine& e, const Dims& D, const double2* xi, const double2* b
       check_finite(e, X, rows * eta, flag);
     }
     if (qtheta && use_qr_pair(rows, cols)) {
-      qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp,
-                        [&](long long r0, long long nr, cudaStream_t st) {
-                          qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st);
-                        });
+      qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp);
       check_finite(e, theta, eta * cols, flag);
       continue;
     }

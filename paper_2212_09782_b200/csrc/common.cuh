@@ -54,6 +54,15 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 
+// gauge phase of reflector column i of a factored QR (R on the upper
+// triangle of a, ld lda): R_ii / |R_ii| (1 when R_ii == 0), the phase
+// gauge_q applies to column i of Q (proj/src/linalg.cpp:25-36)
+__device__ __forceinline__ double2 qr_phase(const double2* __restrict__ a, long long lda, long long i) {
+  const double2 d = a[i * lda + i];
+  const double ad = hypot(d.x, d.y);
+  return ad == 0.0 ? make_double2(1.0, 0.0) : make_double2(d.x / ad, d.y / ad);
+}
+
 // sign flip without touching the FP64 pipe (integer xor on the high word)
 __device__ __forceinline__ double dneg(double x) {
   return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));

@@ -156,8 +156,10 @@ void qr_inplace(Engine& e, double2* a, long long m, long long n, long long lda, 
 
 // The two QRs of one alternating sweep (proj/src/gates.cpp:293-308), pipelined:
 //   QR(X), X (m x k) -- every finished panel p is applied to C (m x nc) on
-//   e.side2, so C <- Q_full^H C, and then `extract(r0, nr, stream)` publishes
-//   rows [r0, r0 + nr) of C, which are final, as columns of Y^H (nc x k);
+//   e.side2, so C <- Q_full^H C, and rows [32p, 32p + 32) of C, final once
+//   panel p is applied, are published as columns of Y^H (nc x k, ld k):
+//   yh[c, i] = ph_i conj(C[i, c]) with ph_i the phase of X's R_ii (the gauge
+//   of Q_m), i.e. Y = Q_m^H C;
 //   QR(Y^H) on e.side3 runs one panel behind: panel p of Y^H starts once block
 //   p is extracted and has received the reflectors of Y^H panels < p
 //   (left-looking block update).
@@ -187,7 +189,6 @@ void pair_form_q(Engine& e, const double2* x, long long m, long long k, double2*
 // and have e.side2 wait for anything that still reads C (C is first written
 // on e.side2).
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
-                       double2* qy, double2* ry,
-                       const std::function<void(long long, long long, cudaStream_t)>& extract);
+                       double2* qy, double2* ry);
 
 }  // namespace qt

@@ -59,14 +59,6 @@ __global__ void inv_norm_kernel(double* dscal, int a, int b, int skip, int out) 
 
 __global__ void zero_flag_kernel(int* f) { *f = 0; }
 
-// gauge phase of reflector column i: R_ii / |R_ii| (1 when R_ii == 0), the
-// phase gauge_q applies to column i of Q (proj/src/linalg.cpp:25-36)
-__device__ __forceinline__ double2 qr_phase(const double2* __restrict__ a, long long lda, long long i) {
-  const double2 d = a[i * lda + i];
-  const double ad = hypot(d.x, d.y);
-  return ad == 0.0 ? make_double2(1.0, 0.0) : make_double2(d.x / ad, d.y / ad);
-}
-
 // Y^H from Q_full^H theta: yh[c, i] = ph_i conj(qt[i, c]) for i < eta, i.e.
 // Y = Q_m^H theta with the gauge-fixed Q_m = Q_raw diag(ph)  (32 x 32 tiles)
 // (rows [ibeg, iend) of qt; yh and the factored X share the leading dimension lda = eta)
@@ -430,10 +422,7 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     ustamp("X");
     if (pair) {
       // both QRs of the sweep in flight at once: QR(Y^H) one panel behind QR(X)
-      qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp,
-                        [&](long long r0, long long nr, cudaStream_t st) {
-                          qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st);
-                        });
+      qr_pair_pipelined(e, X, rows, eta, theta, cols, YH, Qp, Rp);
       if (out.left_iso) {
         // left_iso = Q_m (gates.cpp:373) from X's stored reflectors, on side4
         // concurrently with the tail (Hastings on the main stream)

@@ -1005,11 +1005,51 @@ void pair_form_q(Engine& e, const double2* x, long long m, long long k, double2*
 }
 
 namespace {
+// Rows [j, j + nbp) of H_p^H C and block p of Y^H in one pass over 32-column
+// tiles (replaces three launches on the theta side's critical chain):
+//   W2 = T^H W             (T upper triangular; W2 feeds the C_rest GEMM)
+//   C_top -= V_top W2      (V_top unit lower triangular)
+//   yh[c, j + r] = ph_{j+r} conj(C_top[r, c])   (Y = Q_m^H theta, Q_m gauged)
+__global__ void __launch_bounds__(256) pair_top_kernel(const double2* __restrict__ W, const double2* __restrict__ T,
+                                                       const double2* __restrict__ Vt, long long ldv,
+                                                       double2* __restrict__ ct, long long nc, int nbp,
+                                                       double2* __restrict__ W2, const double2* __restrict__ x,
+                                                       long long k, double2* __restrict__ yh, long long j) {
+  // T and V_top entries are warp-uniform (one row r per warp): broadcast
+  // loads through the read-only path, only the column tiles in shared memory
+  __shared__ double2 ws[NB][NB + 1], w2s[NB][NB + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long c0 = static_cast<long long>(blockIdx.x) * NB, c = c0 + tx;
+  const double2 z = make_double2(0.0, 0.0);
+  for (int r = ty; r < NB; r += 8) ws[r][tx] = (r < nbp && c < nc) ? W[r * nc + c] : z;
+  __syncthreads();
+  for (int r = ty; r < nbp; r += 8) {
+    double2 acc = z;
+    for (int q = 0; q <= r; ++q) {
+      const double2 t = __ldg(&T[q * NB + r]), w = ws[q][tx];  // acc += conj(T[q][r]) W[q]
+      acc.x = fma(t.x, w.x, fma(t.y, w.y, acc.x));
+      acc.y = fma(t.x, w.y, fma(-t.y, w.x, acc.y));
+    }
+    w2s[r][tx] = acc;
+    if (c < nc) W2[r * nc + c] = acc;
+  }
+  __syncthreads();
+  for (int r = ty; r < nbp; r += 8) {
+    if (c < nc) {
+      double2 acc = ct[r * nc + c];
+      for (int q = 0; q <= r; ++q) acc = csub(acc, cmul(__ldg(&Vt[r * ldv + q]), w2s[q][tx]));
+      ct[r * nc + c] = acc;
+      ws[r][tx] = cmul(qr_phase(x, k, j + r), cconj(acc));
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < NB; r += 8)
+    if (c0 + r < nc && tx < nbp) yh[(c0 + r) * k + j + tx] = ws[tx][r];
+}
 }  // namespace
 
 void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2* c, long long nc, double2* yh,
-                       double2* qy, double2* ry,
-                       const std::function<void(long long, long long, cudaStream_t)>& extract) {
+                       double2* qy, double2* ry) {
   if (k == 0) return;
   if (k > m || k > nc || !qr_pair_fits(m, nc)) throw Error(Err::internal, "qr_pair_pipelined: shape not supported");
   const long long npan = ceil_div(k, NB);
@@ -1083,11 +1123,34 @@ void qr_pair_pipelined(Engine& e, double2* x, long long m, long long k, double2*
     QT_CUDA(cudaStreamWaitEvent(sa, e.event(P0 + p), 0));
     // rows [j, j + nbp) of H_p^H C are final first: publish them as block p
     // of Y^H before the rest of C is updated
-    apply_block_reflector(pa.V, kp, pa.T, c + j * nc, nc, m - j, nc, nbp, CW, CW2, gs2, sa, [&] {
-      extract(j, nbp, sa);
+    {
+      // C <- (I - V T V^H)^H C: W = V^H C, then rows of block p (W2 = T^H W,
+      // C_top -= V_top W2, published as block p of Y^H) in one kernel, then
+      // the rest of C (C_rest -= V_rest W2)
+      const long long mp = m - j;
+      GemmDesc g;
+      g.M = nbp; g.N = nc; g.K = mp;
+      g.opA = Op::H; g.A = pa.V; g.lda = kp;
+      g.B = c + j * nc; g.ldb = nc;
+      g.C = CW; g.ldc = nc;
+      zgemm(g, gs2, sa);
+      stamp("thW" + std::to_string(p), sa);
+      pair_top_kernel<<<static_cast<unsigned>(ceil_div(nc, NB)), dim3(NB, 8), 0, sa>>>(
+          CW, pa.T, pa.V, kp, c + j * nc, nc, nbp, CW2, x, k, yh, j);
+      QT_LAUNCHED();
       stamp("extract" + std::to_string(p), sa);
       QT_CUDA(cudaEventRecord(e.event(E0 + p), sa));
-    });
+      if (mp > nbp) {
+        GemmDesc g3;
+        g3.M = mp - nbp; g3.N = nc; g3.K = nbp;
+        g3.A = pa.V + nbp * kp; g3.lda = kp;
+        g3.B = CW2; g3.ldb = nc;
+        g3.C = c + (j + nbp) * nc; g3.ldc = nc;
+        g3.alpha = -1.0; g3.beta = 1.0;
+        zgemm(g3, gs2, sa);
+        stamp("threst" + std::to_string(p), sa);
+      }
+    }
     // ---- X trailing update (look-ahead: next panel's columns on sx, the rest on sxw)
     const long long ntr = k - j - nbp;
     if (ntr > 0) {
