@@ -34,12 +34,7 @@ void Engine::init(int dev, cudaStream_t st) {
   QT_CUDA(cudaMalloc(&barrier, 64 * sizeof(unsigned)));
   QT_CUDA(cudaMemset(barrier, 0, 64 * sizeof(unsigned)));
   QT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-  {
-    // QT_SIDE2_PRIO: 0 = least (default), 1 = one level above, 2 = greatest
-    static const int s2 = std::getenv("QT_SIDE2_PRIO") ? std::atoi(std::getenv("QT_SIDE2_PRIO")) : 0;
-    const int pr = s2 >= 2 ? prio_greatest : (s2 == 1 ? prio_least - 1 : prio_least);
-    QT_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, no_prio ? prio_least : pr));
-  }
+  QT_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   QT_CUDA(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, no_prio ? prio_least : prio_greatest));
   QT_CUDA(cudaStreamCreateWithFlags(&side4, cudaStreamNonBlocking));
   QT_CUDA(cudaStreamCreateWithFlags(&side5, cudaStreamNonBlocking));
