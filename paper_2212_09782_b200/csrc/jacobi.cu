@@ -107,17 +107,6 @@ __device__ __forceinline__ Rot make_rot(double a, double b, double2 c, double to
   // that only two transcendental steps are dependent: with s = |d| + sqrt(..),
   // cs = s / sqrt(s^2 + 4|c|^2) and sn = sign(d) 2|c| / sqrt(s^2 + 4|c|^2);
   // |c| and the phase come from rsqrt(|c|^2) alongside
-#ifdef QT_JACOBI_OLD_ROT
-  {
-    const double inv_ac = rsqrt(ac2);
-    r.e = make_double2(c.x * inv_ac, -c.y * inv_ac);
-    const double theta = (b - a) * 0.5 * inv_ac;
-    const double t = copysign(1.0 / (fabs(theta) + sqrt(fma(theta, theta, 1.0))), theta);
-    r.cs = rsqrt(fma(t, t, 1.0));
-    r.sn = t * r.cs;
-    return r;
-  }
-#endif
   const double d = b - a;
   const double inv_ac = rsqrt(ac2);
   const double s = fabs(d) + sqrt(fma(d, d, 4.0 * ac2));
