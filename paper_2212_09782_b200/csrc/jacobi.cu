@@ -169,7 +169,8 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 
 // C = op(A) B for JX x JX complex tiles in shared memory (row stride JX+1),
 // op(A) = A or A^H, on NW warps with DMMA: each warp owns one 8-row block and
-// BPW 8-column blocks; a complex product is four real MMAs
+// BPW 8-column blocks; a complex product is three real MMAs (3M, as in
+// zgemm.cu: P1 = Re a Re b, P2 = Im a Im b, P3 = (Re a + Im a)(Re b + Im b))
 template <int JX, int NW>
 __device__ __forceinline__ void tile_mm(double2 (*A)[JX + 1], bool conj_t, double2 (*B)[JX + 1],
                                         double2 (*C)[JX + 1]) {
@@ -178,26 +179,26 @@ __device__ __forceinline__ void tile_mm(double2 (*A)[JX + 1], bool conj_t, doubl
   constexpr int WPR = NBLK / BPW;               // warps per block row
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int rb = w / WPR, cb0 = (w % WPR) * BPW;
-  double cre[BPW][2], cim[BPW][2];
+  double p1[BPW][2], p2[BPW][2], p3[BPW][2];
 #pragma unroll
-  for (int b = 0; b < BPW; ++b) cre[b][0] = cre[b][1] = cim[b][0] = cim[b][1] = 0.0;
+  for (int b = 0; b < BPW; ++b) p1[b][0] = p1[b][1] = p2[b][0] = p2[b][1] = p3[b][0] = p3[b][1] = 0.0;
 #pragma unroll 4
   for (int k0 = 0; k0 < JX; k0 += 4) {
     const double2 av = conj_t ? cconj(A[k0 + t][rb * 8 + g]) : A[rb * 8 + g][k0 + t];
+    const double sa = av.x + av.y;
 #pragma unroll
     for (int b = 0; b < BPW; ++b) {
       const double2 bv = B[k0 + t][(cb0 + b) * 8 + g];
-      dmma(cre[b], av.x, bv.x);
-      dmma(cre[b], -av.y, bv.y);
-      dmma(cim[b], av.x, bv.y);
-      dmma(cim[b], av.y, bv.x);
+      dmma(p1[b], av.x, bv.x);
+      dmma(p2[b], av.y, bv.y);
+      dmma(p3[b], sa, bv.x + bv.y);
     }
   }
 #pragma unroll
-  for (int b = 0; b < BPW; ++b) {
-    C[rb * 8 + g][(cb0 + b) * 8 + 2 * t] = make_double2(cre[b][0], cim[b][0]);
-    C[rb * 8 + g][(cb0 + b) * 8 + 2 * t + 1] = make_double2(cre[b][1], cim[b][1]);
-  }
+  for (int b = 0; b < BPW; ++b)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      C[rb * 8 + g][(cb0 + b) * 8 + 2 * t + h] = make_double2(p1[b][h] - p2[b][h], p3[b][h] - (p1[b][h] + p2[b][h]));
 }
 
 template <int JB>
