@@ -693,6 +693,22 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
   by.diag = party + 2 * kNumSMs * NB;
   by.bar = e.barrier + 16;
 
+  // QT_PAIR_DEBUG=1 (eager calls only): timeline of the tall pair on stderr
+  static const bool tdbg = std::getenv("QT_PAIR_DEBUG") != nullptr;
+  static std::vector<cudaEvent_t> tev;
+  std::vector<std::string> tname;
+  auto stamp = [&](const std::string& nm, cudaStream_t st) {
+    if (!tdbg) return;
+    if (tev.size() <= tname.size()) {
+      cudaEvent_t ev;
+      QT_CUDA(cudaEventCreate(&ev));
+      tev.push_back(ev);
+    }
+    QT_CUDA(cudaEventRecord(tev[tname.size()], st));
+    tname.push_back(nm);
+  };
+  stamp("start", sx);
+
   // events: 4000 + 4b: X block b's T ready; +1: X side update done; +2: rows
   // of Y^H block b published; 4000 + 4 nob: start / joins
   const size_t ev0 = 4000, evs = ev0 + 4 * static_cast<size_t>(nob);
@@ -712,12 +728,14 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
     double2* Tb = TOB + b * OB * OB;
     const double2* Vb = V + J * kp + J;
     outer_block_tob(e, V, kp, T, J, w, k, m, Tb, OB, G, G + static_cast<size_t>(OB) * OB, gs, sx);
+    stamp("X" + std::to_string(b), sx);
     QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b), sx));
     // ---- theta side: C <- Q_ob^H C, then rows [J, J + w) of C are final:
     // published as columns [J, J + w) of Y^H
     QT_CUDA(cudaStreamWaitEvent(sa, e.event(ev0 + 4 * b), 0));
     apply_block_reflector(Vb, kp, Tb, c + J * nc, nc, m - J, nc, static_cast<int>(w), CW, CW2, gs2, sa,
-                          [&] { extract(J, w, sa); }, OB, true);
+                          [&] { extract(J, w, sa); stamp("ext" + std::to_string(b), sa); }, OB, true);
+    stamp("th" + std::to_string(b), sa);
     QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b + 2), sa));
     // ---- X look-ahead: the next block's columns on sx, the rest on sxw
     const long long ntr = k - (J + w);
@@ -731,6 +749,7 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
         apply_block_reflector(Vb, kp, Tb, x + J * k + J + w + nn, k, m - J, ntr - nn, static_cast<int>(w), SW, SW2,
                               gss, sxw, nullptr, OB, true);
         QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b + 1), sxw));
+        stamp("Xw" + std::to_string(b), sxw);
         side_last = b;
       }
     }
@@ -764,6 +783,7 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
       gx.alpha = -1.0; gx.beta = 0.0;
       zgemm(gx, gsy, sy);
     }
+    stamp("Y" + std::to_string(b), sy);
   }
   // ---- explicit, gauge-fixed Q and R of Y^H (side3), X's Q if asked (side2)
   set_identity(e, qy, nc, k, k, sy);
@@ -793,6 +813,17 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
   QT_CUDA(cudaStreamWaitEvent(sx, e.event(evs + 1), 0));
   QT_CUDA(cudaEventRecord(e.event(evs + 2), sy));
   QT_CUDA(cudaStreamWaitEvent(sx, e.event(evs + 2), 0));
+  stamp("end", sx);
+  if (tdbg) {
+    QT_CUDA(cudaStreamSynchronize(sx));
+    std::fprintf(stderr, "qr_pair_tall m=%lld k=%lld nc=%lld timeline (us from start):", m, k, nc);
+    for (size_t i = 1; i < tname.size(); ++i) {
+      float ms = 0.f;
+      QT_CUDA(cudaEventElapsedTime(&ms, tev[0], tev[i]));
+      std::fprintf(stderr, " %s=%.0f", tname[i].c_str(), ms * 1000.f);
+    }
+    std::fprintf(stderr, "\n");
+  }
 }
 
 namespace {
