@@ -60,7 +60,8 @@ enum Slot : int {
   S_QR_YW2,
   S_QR_TALL,     //   T of all finished Y^H blocks (k x k, left-looking updates),
   S_QR_TALLZ,    //   the V^H V / Z scratch of its growth,
-  S_QR_PART2,    //   panel scratch
+  S_QR_PART2,    //   panel scratch,
+  S_QR_QYM,      //   T_all V_b^H, forming Q of Y^H block by block
   S_COUNT
 };
 

@@ -637,6 +637,15 @@ void qr_inplace_outer(Engine& e, double2* a, long long m, long long n, long long
   }
 }
 
+namespace {
+// q[(j0 + i) * ld + j0 + i] += 1, i < w (the identity part of a column block
+// of Q = I - V T V^H)
+__global__ void add_diag_kernel(double2* q, long long ld, long long j0, int w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < w) q[(j0 + i) * ld + j0 + i].x += 1.0;
+}
+}  // namespace
+
 bool qr_pair_tall_fits(long long m, long long nc, long long k) {
   static const bool off = std::getenv("QT_NO_TALL_PAIR") != nullptr;
   // both chains on cluster panels (<= 5120 rows): two grid-barrier panels in
@@ -675,6 +684,11 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
   double2* TALL = e.cbuf(S_QR_TALL, static_cast<size_t>(k) * k);
   double2* TZ = e.cbuf(S_QR_TALLZ, static_cast<size_t>(2) * k * OB);
   double2* party = e.cbuf(S_QR_PART2, static_cast<size_t>(2) * kNumSMs * NB + 2 * NB);
+  // Q of Y^H, column block b, on sq right behind Y^H block b (T_all is
+  // left-looking, so Q[:, J:J+w] = E - V[:, :J+w] (T_all[:J+w, :J+w]
+  // V[J:J+w, :J+w]^H) is final once block b is factored)
+  double2* QYM = e.cbuf(S_QR_QYM, static_cast<size_t>(k) * OB);
+  const cudaStream_t sq = e.side5;
   const GemmScratch gs = e.gemm_scratch();
   GemmScratch gss;
   gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
@@ -710,11 +724,13 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
   stamp("start", sx);
 
   // events: 4000 + 4b: X block b's T ready; +1: X side update done; +2: rows
-  // of Y^H block b published; 4000 + 4 nob: start / joins
+  // of Y^H block b published; 4000 + 4 nob: start / joins; + 3 + b: Y^H block
+  // b factored (Q column block b may start); + 3 + nob: Q complete
   const size_t ev0 = 4000, evs = ev0 + 4 * static_cast<size_t>(nob);
   QT_CUDA(cudaEventRecord(e.event(evs), sx));  // everything earlier on sx precedes both side chains
   QT_CUDA(cudaStreamWaitEvent(sy, e.event(evs), 0));
   QT_CUDA(cudaStreamWaitEvent(sa, e.event(evs), 0));
+  QT_CUDA(cudaStreamWaitEvent(sq, e.event(evs), 0));
   QT_CUDA(cudaMemsetAsync(TALL, 0, static_cast<size_t>(k) * k * sizeof(double2), sy));
   // the combined reflector of the finished Y^H blocks is used from row 0: the
   // rows above each block's own diagonal block must be zero
@@ -784,15 +800,31 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
       zgemm(gx, gsy, sy);
     }
     stamp("Y" + std::to_string(b), sy);
+    QT_CUDA(cudaEventRecord(e.event(evs + 3 + b), sy));
+    QT_CUDA(cudaStreamWaitEvent(sq, e.event(evs + 3 + b), 0));
+    {
+      const long long jw = J + w;
+      GemmDesc gm;  // QYM = T_all[:jw, :jw] V[J:jw, :jw]^H  (jw x w)
+      gm.M = jw; gm.N = w; gm.K = jw;
+      gm.A = TALL; gm.lda = k;
+      gm.opB = Op::H; gm.B = Vy + J * kp; gm.ldb = kp;
+      gm.C = QYM; gm.ldc = w;
+      zgemm(gm, GemmScratch{}, sq);
+      GemmDesc gq;  // Q[:, J:jw] = -V[:, :jw] QYM, then + E
+      gq.M = nc; gq.N = w; gq.K = jw;
+      gq.A = Vy; gq.lda = kp;
+      gq.B = QYM; gq.ldb = w;
+      gq.C = qy + J; gq.ldc = k;
+      gq.alpha = -1.0; gq.beta = 0.0;
+      zgemm(gq, GemmScratch{}, sq);
+      add_diag_kernel<<<1, 256, 0, sq>>>(qy, k, J, static_cast<int>(w));
+      QT_LAUNCHED();
+      stamp("Q" + std::to_string(b), sq);
+    }
   }
-  // ---- explicit, gauge-fixed Q and R of Y^H (side3), X's Q if asked (side2)
-  set_identity(e, qy, nc, k, k, sy);
-  for (long long b = nob - 1; b >= 0; --b) {
-    const long long J = b * OB;
-    const long long w = std::min<long long>(OB, k - J);
-    apply_block_reflector(Vy + J * kp + J, kp, TOBy + b * OB * OB, qy + J * k + J, k, nc - J, k - J,
-                          static_cast<int>(w), YW, YW2, gsy, sy, nullptr, OB, false);
-  }
+  // ---- gauge-fixed Q (formed on sq) and R of Y^H (side3), X's Q if asked
+  QT_CUDA(cudaEventRecord(e.event(evs + 3 + nob), sq));
+  QT_CUDA(cudaStreamWaitEvent(sy, e.event(evs + 3 + nob), 0));
   gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
   QT_LAUNCHED();
   gauge_r_kernel<<<grid_for(k * k), 256, 0, sy>>>(yh, k, ry, k, k, k);
