@@ -151,6 +151,17 @@ GemmScratch Engine::gemm_scratch3() {
   return s;
 }
 
+GemmScratch Engine::gemm_scratch4() {
+  GemmScratch s;
+  const size_t part = size_t(1) << 21;
+  s.partial = cbuf(S_GEMM_PART4, part);
+  s.partial_elems = part;
+  const size_t ts = size_t(1) << 16;
+  s.tile_sums = dbuf(S_TILE_SUMS4, ts);
+  s.tile_sums_elems = ts;
+  return s;
+}
+
 // ---------------------------------------------------------------- kernels
 namespace {
 

@@ -62,6 +62,8 @@ enum Slot : int {
   S_QR_TALLZ,    //   the V^H V / Z scratch of its growth,
   S_QR_PART2,    //   panel scratch,
   S_QR_QYM,      //   T_all V_b^H, forming Q of Y^H block by block
+  S_GEMM_PART4,  // split-K scratch of GEMMs on side5 (the tall pair's Q blocks and their consumers)
+  S_TILE_SUMS4,
   S_COUNT
 };
 
@@ -121,6 +123,7 @@ struct Engine {
   GemmScratch gemm_scratch();
   GemmScratch gemm_scratch2();  // separate split-K buffers for GEMMs on side2
   GemmScratch gemm_scratch3();  // ... and on side4
+  GemmScratch gemm_scratch4();  // ... and on side5
 };
 
 // ---- kernels shared by the modules (aux.cu) -------------------------------

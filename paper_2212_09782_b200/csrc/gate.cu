@@ -441,6 +441,9 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
     }
     if (qtheta && qr_pair_tall_fits(rows, cols, eta)) {
       // tall pair: QR(Y^H) one outer block behind QR(X) and the theta application
+      // (the Hastings product stays a single GEMM after the pair: issued per
+      // Q block inside it, it competes with the theta application and the
+      // Y^H chain for the tensor pipe -- north star 7.78 -> 7.62 steps/s)
       qr_pair_tall(e, X, rows, eta, theta, cols, YH, Qp, Rp, out.left_iso ? Qm : nullptr,
                    [&](long long r0, long long nr, cudaStream_t st) {
                      qtheta_yh(e, theta, cols, X, eta, YH, r0, r0 + nr, st);

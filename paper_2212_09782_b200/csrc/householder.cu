@@ -689,6 +689,7 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
   // V[J:J+w, :J+w]^H) is final once block b is factored)
   double2* QYM = e.cbuf(S_QR_QYM, static_cast<size_t>(k) * OB);
   const cudaStream_t sq = e.side5;
+  const GemmScratch gs4 = e.gemm_scratch4();
   const GemmScratch gs = e.gemm_scratch();
   GemmScratch gss;
   gss.partial = e.cbuf(S_GEMM_PARTS, size_t(1) << 22);
@@ -809,15 +810,18 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
       gm.A = TALL; gm.lda = k;
       gm.opB = Op::H; gm.B = Vy + J * kp; gm.ldb = kp;
       gm.C = QYM; gm.ldc = w;
-      zgemm(gm, GemmScratch{}, sq);
+      zgemm(gm, gs4, sq);
       GemmDesc gq;  // Q[:, J:jw] = -V[:, :jw] QYM, then + E
       gq.M = nc; gq.N = w; gq.K = jw;
       gq.A = Vy; gq.lda = kp;
       gq.B = QYM; gq.ldb = w;
       gq.C = qy + J; gq.ldc = k;
       gq.alpha = -1.0; gq.beta = 0.0;
-      zgemm(gq, GemmScratch{}, sq);
+      zgemm(gq, gs4, sq);
       add_diag_kernel<<<1, 256, 0, sq>>>(qy, k, J, static_cast<int>(w));
+      QT_LAUNCHED();
+      // gauge phases of columns [J, jw): R_ii of Y^H, final with block b
+      gauge_q_kernel<<<grid_for(nc * w), 256, 0, sq>>>(yh + J * k + J, k, qy + J, k, nc, w);
       QT_LAUNCHED();
       stamp("Q" + std::to_string(b), sq);
     }
@@ -825,8 +829,6 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
   // ---- gauge-fixed Q (formed on sq) and R of Y^H (side3), X's Q if asked
   QT_CUDA(cudaEventRecord(e.event(evs + 3 + nob), sq));
   QT_CUDA(cudaStreamWaitEvent(sy, e.event(evs + 3 + nob), 0));
-  gauge_q_kernel<<<grid_for(nc * k), 256, 0, sy>>>(yh, k, qy, k, nc, k);
-  QT_LAUNCHED();
   gauge_r_kernel<<<grid_for(k * k), 256, 0, sy>>>(yh, k, ry, k, k, k);
   QT_LAUNCHED();
   if (side_last >= 0) QT_CUDA(cudaStreamWaitEvent(sx, e.event(ev0 + 4 * side_last + 1), 0));
