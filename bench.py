@@ -516,7 +516,7 @@ def gemm_traffic(config):
     """dram__bytes_read.sum + dram__bytes_write.sum of one launch of the
     dominant GEMM of this configuration, from the committed ncu --set full
     captures: north star = the X = theta Y0^H GEMM (5120 x 1024 x 5120,
-    profiles/r02/north_theta_x_raw.csv.gz); C2 = the 1280 x 256 x 1280
+    3M build, profiles/r02_final/gemm_x_raw.csv.gz); C2 = the 1280 x 256 x 1280
     projection (profiles/r01_ncu_full_summary.txt); None when no capture of
     that shape exists."""
     import csv
@@ -524,7 +524,7 @@ def gemm_traffic(config):
     import io
     here = os.path.dirname(os.path.abspath(__file__))
     if config == "north":
-        path = os.path.join(here, "profiles", "r02", "north_theta_x_raw.csv.gz")
+        path = os.path.join(here, "profiles", "r02_final", "gemm_x_raw.csv.gz")
         if not os.path.exists(path):
             return None
         rows = list(csv.reader(io.StringIO(gzip.open(path, "rt").read())))

@@ -63,3 +63,27 @@ def test_zgemm_split_k_deterministic(ctx):
         outs.append(tc.numpy())
     assert rel(outs[0], a.conj().T @ b) < 1e-13
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("opa,opb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_zgemm_3m_unbalanced_parts(ctx, opa, opb):
+    """The 3M products (Im c = P3 - P1 - P2) keep the normwise bound
+    |dC| <= c u |A||B| K even when real and imaginary parts differ by orders
+    of magnitude, and real inputs give exactly real outputs."""
+    rng = np.random.default_rng(31 + 2 * opa + opb)
+    m, n, k = 300, 260, 700
+    a = rng.standard_normal((m, k)) + 1j * 1e-4 * rng.standard_normal((m, k))
+    b = 1e-3 * rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
+    ast, bst = op(a, opa), op(b, opb)  # stored so that op(stored) = a, b
+    ta, tb, tc = ctx.tensor(ast.copy()), ctx.tensor(bst.copy()), ctx.tensor(np.zeros((m, n)) + 0j)
+    zgemm(ctx, opa, opb, m, n, k, ta.ptr, ast.shape[1], tb.ptr, bst.shape[1], tc.ptr, n, alpha=1.0, beta=0.0)
+    ref = a @ b
+    bound = np.abs(a).max() * np.abs(b).max() * k * 2.2e-16
+    assert np.abs(tc.numpy() - ref).max() < 4 * bound
+    # real operands: the imaginary parts cancel exactly (P3 and P1 see the same inputs)
+    ar, br = rng.standard_normal((m, k)) + 0j, rng.standard_normal((k, n)) + 0j
+    ta, tb = ctx.tensor(op(ar, opa).copy()), ctx.tensor(op(br, opb).copy())
+    zgemm(ctx, opa, opb, m, n, k, ta.ptr, m if opa else k, tb.ptr, k if opb else n, tc.ptr, n, alpha=1.0, beta=0.0)
+    out = tc.numpy()
+    assert np.all(out.imag == 0.0)
+    assert rel(out, ar @ br) < 1e-14
