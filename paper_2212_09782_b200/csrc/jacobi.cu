@@ -246,12 +246,22 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   auto jslot = [&](long long g, int p) { return a.Jbuf + ((g & 1) * P + p) * static_cast<long long>(JX * JX); };
   auto phase_a = [&](long long g, int round, int p) {
     const int bI = rr_slot(p, round, nb), bJ = rr_slot(nb - 1 - p, round, nb);
-    for (int e = tid; e < JX * JX; e += JT) {
-      const int i = e / JX, j = e % JX;
-      const int gi = (i < JB ? bI * JB + i : bJ * JB + i - JB);
-      const int gj = (j < JB ? bI * JB + j : bJ * JB + j - JB);
-      S[i][j] = a.G[static_cast<long long>(gi) * N + gj];
-      Jm[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    {
+      constexpr int PER = JX * JX / JT;
+      double2 rs[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {  // all loads in flight at once
+        const int e = tid + k * JT, i = e / JX, j = e % JX;
+        const int gi = (i < JB ? bI * JB + i : bJ * JB + i - JB);
+        const int gj = (j < JB ? bI * JB + j : bJ * JB + j - JB);
+        rs[k] = a.G[static_cast<long long>(gi) * N + gj];
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * JT, i = e / JX, j = e % JX;
+        S[i][j] = rs[k];
+        Jm[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+      }
     }
     __syncthreads();
     // inner sweep over the 2JB local indices: JB "cross" rounds pairing I
@@ -320,19 +330,38 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
       xJ = rr_slot(nb - 1 - xa, round, nb);
     }
     double2* M = isG ? a.G : a.V;
-    for (int e = tid; e < JX * JX; e += JT) {
-      const int i = e / JX, j = e % JX;
+    // the item's global loads issue at once (tile, Jy and, for JB = 16, Jx
+    // staged in registers): one L2 round trip instead of a dependent chain per
+    // loop iteration (JB = 32 fetches Jx after the first product: 24 staged
+    // values per thread would spill at 128 registers)
+    constexpr int PER = JX * JX / JT;
+    constexpr bool STAGE_JX = PER <= 4;
+    double2 rs[PER], rj[PER], rx[STAGE_JX ? PER : 1];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = tid + k * JT, i = e / JX, j = e % JX;
       const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
       const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
-      S[i][j] = M[static_cast<long long>(gi) * N + gj];
-      Jm[i][j] = jy[e];
+      rs[k] = M[static_cast<long long>(gi) * N + gj];
+      rj[k] = jy[e];
+      if (STAGE_JX) rx[STAGE_JX ? k : 0] = isG ? jx[e] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = tid + k * JT;
+      S[e / JX][e % JX] = rs[k];
+      Jm[e / JX][e % JX] = rj[k];
     }
     __syncthreads();
     // T1 = S Jy, then (G tiles) out = Jx^H T1, on the FP64 tensor pipe
     tile_mm<JX, JT / 32>(S, false, Jm, T1);
     __syncthreads();
     if (isG) {
-      for (int e = tid; e < JX * JX; e += JT) Jm[e / JX][e % JX] = jx[e];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * JT;
+        Jm[e / JX][e % JX] = STAGE_JX ? rx[STAGE_JX ? k : 0] : jx[e];
+      }
       __syncthreads();
       tile_mm<JX, JT / 32>(Jm, true, T1, S);
       __syncthreads();
@@ -351,6 +380,20 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
         const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
         M[static_cast<long long>(gj) * N + gi] = cconj(O[i][j]);
       }
+    __syncthreads();
+  };
+  // the diagonal pair tile (x, x) of round g IS the rotated subproblem phase
+  // A(g) leaves in shared memory (J^H G[X,X] J up to rounding): written back
+  // by the solving CTA itself -- no other item of round g - 1 or g touches
+  // those three block pairs -- so round g needs no diagonal tile update
+  auto store_diag = [&](int round, int p) {
+    const int bI = rr_slot(p, round, nb), bJ = rr_slot(nb - 1 - p, round, nb);
+    for (int e = tid; e < JX * JX; e += JT) {
+      const int i = e / JX, j = e % JX;
+      const int gi = (i < JB ? bI * JB + i : bJ * JB + i - JB);
+      const int gj = (j < JB ? bI * JB + j : bJ * JB + j - JB);
+      a.G[static_cast<long long>(gi) * N + gj] = S[i][j];
+    }
     __syncthreads();
   };
   // publish a G tile of global round rg (release after the CTA's stores)
@@ -375,7 +418,10 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   // CTA x, and one off-diagonal tile per next pair, CTAs P..) go first and are
   // flagged; the CTAs < P wait for their three tiles and solve; the other
   // CTAs finish the remaining tiles; one grid barrier per round.
-  if (cta < P) phase_a(0, 0, cta);
+  if (cta < P) {
+    phase_a(0, 0, cta);
+    store_diag(0, cta);
+  }
   jgrid_sync(a.bar, G, epoch);
   int sw = 0, rd = 0;
   bool conv = false;
@@ -396,10 +442,6 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
       const int y2 = pair_of(partner(rr_slot(nb - 1 - x, rd, nb), nr), rd);
       return y == y1 || y == y2;
     };
-    if (cta < P) {
-      tile(gcur, rd, true, cta, cta, 0);
-      if (doA) flag_tile(cta, cta, rg);
-    }
     if (doA && cta >= P)
       for (int q = cta - P; q < P; q += G - P) {
         int x, y;
@@ -419,12 +461,16 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     if (doA && cta < P) {
       int x, y;
       crit(cta, x, y);
-      wait_tile(x, x, rg);
-      wait_tile(y, y, rg);
+      // the diagonal tiles (x, x) and (y, y) of round gcur were written by
+      // the solves of the previous iteration (before the grid barrier)
       if (x != y) wait_tile(x, y, rg);
       __syncthreads();
       long long t2 = stamp ? clock64() : 0;
       phase_a(gcur + 1, nr, cta);
+      // at a sweep end the solve is speculative: its diagonal tile is
+      // written only once the convergence scan (which must see the end of
+      // this sweep) has decided to go on
+      if (rd != R1 - 1) store_diag(nr, cta);
       if (stamp) {
         pw += t2 - t1;
         pa += clock64() - t2;
@@ -487,6 +533,10 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
         sw = ns;
         break;
       }
+      // going on: the deferred diagonal tiles, visible to every solve of the
+      // next round (which reads them without a flag) after one more barrier
+      if (cta < P) store_diag(nr, cta);
+      jgrid_sync(a.bar, G, epoch);
     }
     if (stamp) ps += clock64() - t3 + (t1 - t0);
     sw = ns;
