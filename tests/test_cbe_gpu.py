@@ -19,7 +19,7 @@ def block_of(xi, b_m, b_n):
     return np.einsum("xa,iag,jgc->xijc", xi, b_m, b_n)
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 16, 33, 100, 257, 356])
+@pytest.mark.parametrize("n", [1, 2, 5, 16, 33, 100, 257, 356, 513, 1100])  # JB = 16 and 32
 def test_eigh_matches_lapack(ctx, n):
     rng = np.random.default_rng(n)
     a = crand(rng, n, n)
