@@ -120,7 +120,7 @@ GemmScratch Engine::gemm_scratch() {
   GemmScratch s;
   // split-K partials: enough for every split configuration the dispatcher
   // picks on the hot-path shapes; it falls back to fewer splits otherwise
-  const size_t part = size_t(1) << 22;  // 4M complex = 64 MB
+  const size_t part = size_t(1) << 24;  // 16M complex = 256 MB (a 2-way split of 5120 x 1024 outputs)
   s.partial = cbuf(S_GEMM_PART, part);
   s.partial_elems = part;
   const size_t ts = size_t(1) << 20;

@@ -88,6 +88,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+// 4-D box over chunked operands: {16 doubles, rows, chunks, batch}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z,
+                                            int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(d0), "+d"(d1)
@@ -101,6 +110,7 @@ struct KParams {
   long long M, N, K;
   int splits, kt_per_split;
   int a_bz, b_bz;  // 1: operand is batched, 0: shared by every batch entry
+  int a4, b4;      // 1: the strided-chunk operand (op(A) = A^H, op(B) = B) has a 4-D map: one TMA per stage
   double2* C;
   long long ldc, strideC, rsplit, ldc_hi;
   double alpha, beta;
@@ -180,12 +190,16 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
 #pragma unroll
       for (int c = 0; c < BK / 8; ++c)
         tma_load_3d(As + c * BM * 128, &tmA, &full[s], 2 * (k0 + 8 * c), (int)m0, za);
+    } else if (p.a4) {
+      tma_load_4d(As, &tmA, &full[s], 0, k0, (int)m0 / 8, za);
     } else {
 #pragma unroll
       for (int c = 0; c < BM / 8; ++c)
         tma_load_3d(As + c * BK * 128, &tmA, &full[s], 2 * ((int)m0 + 8 * c), k0, za);
     }
-    if (OPB == 0) {
+    if (OPB == 0 && p.b4) {
+      tma_load_4d(Bs, &tmB, &full[s], 0, k0, (int)n0 / 8, zb);
+    } else if (OPB == 0) {
 #pragma unroll
       for (int c = 0; c < BN / 8; ++c)
         tma_load_3d(Bs + c * BK * 128, &tmB, &full[s], 2 * ((int)n0 + 8 * c), k0, zb);
@@ -448,6 +462,33 @@ CUtensorMap make_map(const double2* base, long long contig, long long rows, long
   return m;
 }
 
+// 4-D map over a batch of row-major complex matrices whose contiguous axis is
+// cut into 8-element (128-byte) chunks: dim0 = 16 doubles, dim1 = rows
+// (stride ld), dim2 = chunks (stride 128 B), dim3 = batch; one box = box_rows
+// x box_chunks chunk blocks, laid out in shared memory exactly like box_chunks
+// 3-D boxes side by side (chunk-major, 1 KB-aligned blocks: same swizzle).
+// Needs contig % 8 == 0 (a ragged last chunk would read past the row).
+CUtensorMap make_map4(const double2* base, long long contig, long long rows, long long ld, int batch,
+                      long long bstride, int box_rows, int box_chunks) {
+  CUtensorMap m;
+  if (batch <= 1) bstride = ld * (rows > 0 ? rows : 1);
+  cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(contig / 8),
+                        static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 16, 128, static_cast<cuuint64_t>(bstride) * 16};
+  cuuint32_t box[4] = {16, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_chunks), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(base), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (4-D) failed (%d): contig=%lld rows=%lld ld=%lld batch=%d",
+                  static_cast<int>(r), contig, rows, ld, batch);
+    throw Error(Err::cuda, buf);
+  }
+  return m;
+}
+
 template <int OPA, int OPB, int WGM, int WGN, int WTM, int WTN, int BK, int STAGES, int MODE>
 void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double* resid_out) {
   using C_ = Cfg<OPA, OPB, WGM, WGN, WTM, WTN, BK, STAGES>;
@@ -460,10 +501,18 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
   const int a_bz = (d.batch > 1 && d.strideA != 0) ? 1 : 0;
   const int b_bz = (d.batch > 1 && d.strideB != 0) ? 1 : 0;
   const int ba = a_bz ? d.batch : 1, bb = b_bz ? d.batch : 1;
+  // the strided-chunk operands (op(A) = A^H: chunks along m; op(B) = B:
+  // chunks along n) take one 4-D TMA per stage instead of BM/8 or BN/8 3-D
+  // ones when their contiguous extent is a multiple of 8
+  static const bool no4 = std::getenv("QT_GEMM_NO_TMA4D") != nullptr;
+  const bool a4 = OPA == 1 && !no4 && d.M % 8 == 0;
+  const bool b4 = OPB == 0 && !no4 && d.N % 8 == 0;
   const CUtensorMap tA = (OPA == 0) ? make_map(d.A, d.K, d.M, d.lda, ba, d.strideA, BM)
+                         : a4       ? make_map4(d.A, d.M, d.K, d.lda, ba, d.strideA, BK, BM / 8)
                                     : make_map(d.A, d.M, d.K, d.lda, ba, d.strideA, BK);
-  const CUtensorMap tB = (OPB == 0) ? make_map(d.B, d.N, d.K, d.ldb, bb, d.strideB, BK)
-                                    : make_map(d.B, d.K, d.N, d.ldb, bb, d.strideB, BN);
+  const CUtensorMap tB = (OPB == 1) ? make_map(d.B, d.K, d.N, d.ldb, bb, d.strideB, BN)
+                         : b4       ? make_map4(d.B, d.N, d.K, d.ldb, bb, d.strideB, BK, BN / 8)
+                                    : make_map(d.B, d.N, d.K, d.ldb, bb, d.strideB, BK);
   const long long tiles_m = ceil_div(d.M, BM), tiles_n = ceil_div(d.N, BN);
   const int nkt = static_cast<int>(ceil_div(d.K, BK));
   int splits = d.splits;
@@ -487,6 +536,8 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
   p.kt_per_split = kt_per > 0 ? kt_per : 1;
   p.a_bz = a_bz;
   p.b_bz = b_bz;
+  p.a4 = a4 ? 1 : 0;
+  p.b4 = b4 ? 1 : 0;
   p.C = d.C;
   p.ldc = d.ldc;
   p.strideC = d.strideC;
@@ -564,9 +615,11 @@ void dispatch_shape(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, do
   for (int c = 0; c < 4; ++c) {
     if (!cands[c].ok) continue;
     const long long tiles = ceil_div(d.M, cands[c].bm) * ceil_div(d.N, cands[c].bn) * d.batch;
-    // split-K only for products whose unsplit tiling is at most two waves
-    // (large products: the partial traffic outweighs the last-wave imbalance)
-    const bool may_split = tiles < 2 * kNumSMs;
+    // split-K for products of up to eight waves: below two the imbalance of
+    // the last wave dominates; up to eight a 2-4 way split still beats a
+    // mostly empty last wave (north-star X and Hastings, 640 tiles = 4.3
+    // waves: 5 rounds unsplit, 9 rounds of half the K split two ways)
+    const bool may_split = tiles < 8 * kNumSMs;
     for (int sp = 1; sp <= 16; ++sp) {
       if (sp > 1 && (!may_split || MODE == 1 || d.splits > 0 || fixed_split || nkt / sp < 4 ||
                      static_cast<size_t>(sp) * d.batch * d.M * d.N > s.partial_elems))
