@@ -110,7 +110,7 @@ struct KParams {
   long long M, N, K;
   int splits, kt_per_split;
   int a_bz, b_bz;  // 1: operand is batched, 0: shared by every batch entry
-  int a4, b4;      // 1: the strided-chunk operand (op(A) = A^H, op(B) = B) has a 4-D map: one TMA per stage
+  int a4, b4;      // 1: the operand has a 4-D chunked map: one TMA per stage
   double2* C;
   long long ldc, strideC, rsplit, ldc_hi;
   double alpha, beta;
@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
     uint8_t* Bs = As + A_BYTES;
     const int k0 = (kt_begin + it) * BK;
     const int za = b * p.a_bz, zb = b * p.b_bz;
-    if (OPA == 0) {
+    if (OPA == 0 && p.a4) {
+      tma_load_4d(As, &tmA, &full[s], 0, (int)m0, k0 / 8, za);
+    } else if (OPA == 0) {
 #pragma unroll
       for (int c = 0; c < BK / 8; ++c)
         tma_load_3d(As + c * BM * 128, &tmA, &full[s], 2 * (k0 + 8 * c), (int)m0, za);
@@ -203,6 +205,8 @@ __global__ void __launch_bounds__(WGM * WGN * 32, 1)
 #pragma unroll
       for (int c = 0; c < BN / 8; ++c)
         tma_load_3d(Bs + c * BK * 128, &tmB, &full[s], 2 * ((int)n0 + 8 * c), k0, zb);
+    } else if (p.b4) {
+      tma_load_4d(Bs, &tmB, &full[s], 0, (int)n0, k0 / 8, zb);
     } else {
 #pragma unroll
       for (int c = 0; c < BK / 8; ++c)
@@ -504,15 +508,18 @@ void launch_cfg(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, double
   // the strided-chunk operands (op(A) = A^H: chunks along m; op(B) = B:
   // chunks along n) take one 4-D TMA per stage instead of BM/8 or BN/8 3-D
   // ones when their contiguous extent is a multiple of 8
+  // (likewise the K-contiguous operands: BK/8 = 2 -> 1 copies)
   static const bool no4 = std::getenv("QT_GEMM_NO_TMA4D") != nullptr;
-  const bool a4 = OPA == 1 && !no4 && d.M % 8 == 0;
-  const bool b4 = OPB == 0 && !no4 && d.N % 8 == 0;
-  const CUtensorMap tA = (OPA == 0) ? make_map(d.A, d.K, d.M, d.lda, ba, d.strideA, BM)
-                         : a4       ? make_map4(d.A, d.M, d.K, d.lda, ba, d.strideA, BK, BM / 8)
-                                    : make_map(d.A, d.M, d.K, d.lda, ba, d.strideA, BK);
-  const CUtensorMap tB = (OPB == 1) ? make_map(d.B, d.K, d.N, d.ldb, bb, d.strideB, BN)
-                         : b4       ? make_map4(d.B, d.N, d.K, d.ldb, bb, d.strideB, BK, BN / 8)
-                                    : make_map(d.B, d.N, d.K, d.ldb, bb, d.strideB, BK);
+  const bool a4 = !no4 && (OPA == 1 ? d.M : d.K) % 8 == 0;
+  const bool b4 = !no4 && (OPB == 0 ? d.N : d.K) % 8 == 0;
+  const CUtensorMap tA = OPA == 0 ? (a4 ? make_map4(d.A, d.K, d.M, d.lda, ba, d.strideA, BM, BK / 8)
+                                        : make_map(d.A, d.K, d.M, d.lda, ba, d.strideA, BM))
+                                  : (a4 ? make_map4(d.A, d.M, d.K, d.lda, ba, d.strideA, BK, BM / 8)
+                                        : make_map(d.A, d.M, d.K, d.lda, ba, d.strideA, BK));
+  const CUtensorMap tB = OPB == 1 ? (b4 ? make_map4(d.B, d.K, d.N, d.ldb, bb, d.strideB, BN, BK / 8)
+                                        : make_map(d.B, d.K, d.N, d.ldb, bb, d.strideB, BN))
+                                  : (b4 ? make_map4(d.B, d.N, d.K, d.ldb, bb, d.strideB, BK, BN / 8)
+                                        : make_map(d.B, d.N, d.K, d.ldb, bb, d.strideB, BK));
   const long long tiles_m = ceil_div(d.M, BM), tiles_n = ceil_div(d.N, BN);
   const int nkt = static_cast<int>(ceil_div(d.K, BK));
   int splits = d.splits;
