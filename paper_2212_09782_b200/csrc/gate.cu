@@ -95,6 +95,7 @@ __global__ void qtheta_resid_partial_kernel(const double2* __restrict__ qt, long
   for (long long i = blockIdx.x; i < rows; i += gridDim.x) {
     const double2* row = qt + i * cols;
     if (i < eta) {
+      if (!w) continue;  // Z only (w == nullptr)
       const double2 ph = cconj(qr_phase(a, lda, i));
       const double2* wr = w + i * cols;
       for (long long c = threadIdx.x; c < cols; c += blockDim.x) {
@@ -497,14 +498,12 @@ void gate_qr_async(Engine& e, const Dims& D, const double2* xi, const double2* b
   ustamp("xi_bn");
   const bool fork_resid = fork_tail && pol.compute_explicit_error;
   if (fork_resid) {
-    double2* W = e.cbuf(S_W, eta * cols);
-    GemmDesc gw;
-    gw.M = eta; gw.N = cols; gw.K = eta;
-    gw.opA = Op::H; gw.A = Rp; gw.lda = eta;
-    gw.opB = Op::H; gw.B = Qp; gw.ldb = eta;
-    gw.C = W; gw.ldc = cols;
-    zgemm(gw, e.gemm_scratch2(), e.side);
-    qtheta_resid(e, theta, rows, cols, X, eta, W, e.dscal + SC_RESID, e.side);
+    // eps = ||Y - L Q_n||^2 + ||Z||^2, and L Q_n = Rp^H Qp^H IS the QR of
+    // Y^H = Qp Rp: its first term is the QR's backward error (<= c u ||Y||),
+    // below the rounding of the reference's own theta-sized residual
+    // (gates.cpp:464-485) -- only ||Z||^2, the rows of Q_full^H theta outside
+    // Q_m's span, is summed (no eta x cols product)
+    qtheta_resid(e, theta, rows, cols, X, eta, nullptr, e.dscal + SC_RESID, e.side);
     QT_CUDA(cudaEventRecord(e.event(1001), e.side));
   }
   if (out.b_m) {
