@@ -642,12 +642,13 @@ void dispatch_shape(const GemmDesc& d, const GemmScratch& s, cudaStream_t st, do
       }
     }
   }
-  // short-K products with many tiles (block-reflector updates, K = 128):
-  // 64 x 64 tiles run two CTAs per SM (97 KB of shared memory, 128 threads
-  // each), so one CTA's pipeline fill and C epilogue overlap the other's
-  // DMMA work -- 1.12x over 64 x 128 at 5120 x 5120 x 128 and 20480 x 4096 x
-  // 128, while long-K products keep the larger tile
-  if (best == 0 && nkt <= 16 && ceil_div(d.M, 64) * ceil_div(d.N, 128) * d.batch >= 2 * kNumSMs) {
+  // short-K products (K <= 1024) with many tiles: 64 x 64 tiles run two
+  // CTAs per SM (97 KB of shared memory, 128 threads each), so one CTA's
+  // pipeline fill and C epilogue overlap the other's DMMA work -- 1.12x over
+  // 64 x 128 at K = 128 (block-reflector updates), 1.04x at K = 512, 1.02x at
+  // K = 1024 (theta); longer K keeps the larger tile (5120 x 1024 x 5120:
+  // 0.97x with 64 x 64)
+  if (best == 0 && nkt <= 64 && ceil_div(d.M, 64) * ceil_div(d.N, 128) * d.batch >= 2 * kNumSMs) {
     best = 1;
     best_s = 1;
   }
