@@ -66,7 +66,7 @@ struct JacobiArgs {
   double abs_floor;  // rotations skipped below abs_floor * ||G||_F
   int* sweeps_out;
   long long* prof;  // optional: cycles of CTA 0 in phase A / flag waits / phase B / first wave + barrier
-  unsigned* tflag;  // [P(P+1)/2] round counter of the last update of every G pair tile
+  unsigned* tflag;  // [P(P+1)/2][2] round counter of the last update of every critical pair tile half
   const double* fro2;  // ||G||_F^2 (device)
 };
 
@@ -171,14 +171,17 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // op(A) = A or A^H, on NW warps with DMMA: each warp owns one 8-row block and
 // BPW 8-column blocks; a complex product is three real MMAs (3M, as in
 // zgemm.cu: P1 = Re a Re b, P2 = Im a Im b, P3 = (Re a + Im a)(Re b + Im b))
-template <int JX, int NW>
+// HALF: only the output columns [hc JX/2, (hc + 1) JX/2) (one column block
+// of the pair), on all warps
+template <int JX, int NW, bool HALF = false>
 __device__ __forceinline__ void tile_mm(double2 (*A)[JX + 1], bool conj_t, double2 (*B)[JX + 1],
-                                        double2 (*C)[JX + 1]) {
+                                        double2 (*C)[JX + 1], int hc = 0) {
   constexpr int NBLK = JX / 8;                  // 8x8 blocks per dimension
-  constexpr int BPW = NBLK * NBLK / NW;         // blocks per warp
-  constexpr int WPR = NBLK / BPW;               // warps per block row
+  constexpr int NBC = HALF ? NBLK / 2 : NBLK;   // output column blocks
+  constexpr int BPW = NBLK * NBC / NW;          // blocks per warp
+  constexpr int WPR = NBC / BPW;                // warps per block row
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int rb = w / WPR, cb0 = (w % WPR) * BPW;
+  const int rb = w / WPR, cb0 = (w % WPR) * BPW + (HALF ? hc * NBC : 0);
   double p1[BPW][2], p2[BPW][2], p3[BPW][2];
 #pragma unroll
   for (int b = 0; b < BPW; ++b) p1[b][0] = p1[b][1] = p2[b][0] = p2[b][1] = p3[b][0] = p3[b][1] = 0.0;
@@ -320,7 +323,9 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
   };
 
   // ---- phase B work item: G pair tile (xa <= yb) or V row chunk rc
-  auto tile = [&](long long g, int round, bool isG, int xa, int yb, int rc) {
+  // hc >= 0 (G tiles): only the columns of block hc of pair yb (and their
+  // mirrored rows) -- a critical tile split over two CTAs
+  auto tile = [&](long long g, int round, bool isG, int xa, int yb, int rc, int hc = -1) {
     const double2* jy = jslot(g, yb);
     const double2* jx = jslot(g, xa < 0 ? 0 : xa);
     const int yI = rr_slot(yb, round, nb), yJ = rr_slot(nb - 1 - yb, round, nb);
@@ -354,7 +359,10 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     }
     __syncthreads();
     // T1 = S Jy, then (G tiles) out = Jx^H T1, on the FP64 tensor pipe
-    tile_mm<JX, JT / 32>(S, false, Jm, T1);
+    if (hc >= 0)
+      tile_mm<JX, JT / 32, true>(S, false, Jm, T1, hc);
+    else
+      tile_mm<JX, JT / 32>(S, false, Jm, T1);
     __syncthreads();
     if (isG) {
 #pragma unroll
@@ -363,19 +371,23 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
         Jm[e / JX][e % JX] = STAGE_JX ? rx[STAGE_JX ? k : 0] : jx[e];
       }
       __syncthreads();
-      tile_mm<JX, JT / 32>(Jm, true, T1, S);
+      if (hc >= 0)
+        tile_mm<JX, JT / 32, true>(Jm, true, T1, S, hc);
+      else
+        tile_mm<JX, JT / 32>(Jm, true, T1, S);
       __syncthreads();
     }
     double2(*O)[JX + 1] = isG ? S : T1;
-    for (int e = tid; e < JX * JX; e += JT) {
-      const int i = e / JX, j = e % JX;
+    const int jlo = hc >= 0 ? hc * JB : 0, jw = hc >= 0 ? JB : JX;
+    for (int e = tid; e < JX * jw; e += JT) {
+      const int i = e / jw, j = jlo + e % jw;
       const int gi = isG ? (i < JB ? xI * JB + i : xJ * JB + i - JB) : rc * JX + i;
       const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
       M[static_cast<long long>(gi) * N + gj] = O[i][j];
     }
     if (isG && xa != yb)
-      for (int e = tid; e < JX * JX; e += JT) {  // mirror, coalesced along i
-        const int j = e / JX, i = e % JX;
+      for (int e = tid; e < JX * jw; e += JT) {  // mirror, coalesced along i
+        const int j = jlo + e / JX, i = e % JX;
         const int gi = i < JB ? xI * JB + i : xJ * JB + i - JB;
         const int gj = j < JB ? yI * JB + j : yJ * JB + j - JB;
         M[static_cast<long long>(gj) * N + gi] = cconj(O[i][j]);
@@ -397,20 +409,22 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
     __syncthreads();
   };
   // publish a G tile of global round rg (release after the CTA's stores)
-  auto flag_tile = [&](int x, int y, unsigned rg) {
+  // (one flag per column half of a critical tile: the halves run on two CTAs)
+  auto flag_tile = [&](int x, int y, int hc, unsigned rg) {
     if (tid == 0) {
       __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tflag + tidx(x, y)), "r"(rg) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tflag + 2 * tidx(x, y) + hc), "r"(rg) : "memory");
     }
   };
   auto wait_tile = [&](int x, int y, unsigned rg) {
-    if (tid == 0) {
-      const unsigned* f = a.tflag + tidx(min(x, y), max(x, y));
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      } while (v < rg);
-    }
+    if (tid == 0)
+      for (int hc = 0; hc < 2; ++hc) {
+        const unsigned* f = a.tflag + 2 * tidx(min(x, y), max(x, y)) + hc;
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        } while (v < rg);
+      }
   };
   // ---- schedule: phase A of round 0, barrier; then every iteration runs
   // phase B of round (sw, rd) and, overlapped with it, phase A of the next
@@ -443,7 +457,8 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
       return y == y1 || y == y2;
     };
     if (doA && cta >= P)
-      for (int q = cta - P; q < P; q += G - P) {
+      for (int u = cta - P; u < 2 * P; u += G - P) {  // (next pair, column half)
+        const int q = u >> 1, hc = u & 1;
         int x, y;
         crit(q, x, y);
         if (x == y) continue;
@@ -454,8 +469,8 @@ __global__ void __launch_bounds__(JB * 16) jacobi_kernel(JacobiArgs a) {
                                                                 : rr_slot(pair_of(b1, rd), rd, nb);
         const int o2 = partner(o1, nr);  // the other block of pair(b1) meets o2 in the next round
         if (o2 != b2 && pair_of(o2, rd) == pair_of(b2, rd) && pair_of(o1, nr) < q) continue;
-        tile(gcur, rd, true, x, y, 0);
-        flag_tile(x, y, rg);
+        tile(gcur, rd, true, x, y, 0, hc);
+        flag_tile(x, y, hc, rg);
       }
     long long t1 = stamp ? clock64() : 0;
     if (doA && cta < P) {
@@ -716,12 +731,12 @@ const EighStatus* eigh_device(Engine& e, const double2* h, long long n, double* 
   const int ngt = npairs * (npairs + 1) / 2;
   const int grid = std::min(e.num_sms, std::max(2 * npairs, std::min(ngt + (N / JX) * npairs, e.num_sms)));
   if (grid <= npairs) throw Error(Err::capacity, "eigh: matrix too large for the cooperative Jacobi kernel");
-  // [cta_max 2 grid][sweeps 8][tflag ngt/2+1][sorted index n/2+1] (doubles)
-  double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8 + ngt / 2 + 1 + static_cast<size_t>(n) / 2 + 2);
+  // [cta_max 2 grid][sweeps 8][tflag: 2 halves x ngt -> ngt+1][sorted index n/2+1] (doubles)
+  double* cta_max = e.dbuf(S_MISC, 2 * static_cast<size_t>(grid) + 8 + ngt + 1 + static_cast<size_t>(n) / 2 + 2);
   int* sweeps = reinterpret_cast<int*>(cta_max + 2 * grid);
   unsigned* tflag = reinterpret_cast<unsigned*>(cta_max + 2 * grid + 8);
   jacobi_setup_kernel<<<static_cast<int>(std::min<long long>(ceil_div(static_cast<long long>(N) * N, 256), 2048)), 256,
-                        0, e.stream>>>(h, static_cast<int>(n), N, fro, G, V, e.barrier + 8, tflag, ngt);
+                        0, e.stream>>>(h, static_cast<int>(n), N, fro, G, V, e.barrier + 8, tflag, 2 * ngt);
   QT_LAUNCHED();
   JacobiArgs a;
   a.G = G;
@@ -793,7 +808,7 @@ const EighStatus* eigh_device(Engine& e, const double2* h, long long n, double* 
   std::call_once(attr_once, [] {
     QT_CUDA(cudaFuncSetAttribute(jacobi_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   });
-  int* idx = reinterpret_cast<int*>(cta_max + 2 * grid + 8 + ngt / 2 + 1);
+  int* idx = reinterpret_cast<int*>(cta_max + 2 * grid + 8 + ngt + 1);
   jacobi_sort_kernel<<<1, 1024, smem, e.stream>>>(G, static_cast<int>(n), N, fro, w, idx);
   QT_LAUNCHED();
   const long long nn = static_cast<long long>(n) * n;
