@@ -3,7 +3,7 @@
 # update and one step, and --set full captures of the dominant kernels at the
 # north-star shapes (each command first exits 0 without ncu).
 set -o pipefail
-P=gpurun_out/r02f2
+P=gpurun_out/r02f3
 mkdir -p $P
 python tools/profile_update.py --config north > $P/pu.log 2>&1 && \
 N0=$(grep -o "launches_before=[0-9]*" $P/pu.log | cut -d= -f2) && NP=$(grep -o "launches_profiled=[0-9]*" $P/pu.log | cut -d= -f2) && \
