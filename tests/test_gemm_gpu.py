@@ -87,3 +87,25 @@ def test_zgemm_3m_unbalanced_parts(ctx, opa, opb):
     out = tc.numpy()
     assert np.all(out.imag == 0.0)
     assert rel(out, ar @ br) < 1e-14
+
+
+@pytest.mark.parametrize("opa,opb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("m,n,k", [(64, 256, 1024), (200, 136, 88), (1280, 1280, 32), (520, 96, 5120),
+                                   (72, 24, 40)])
+def test_zgemm_chunked_maps_batched(ctx, opa, opb, m, n, k):
+    """4-D chunked tensor maps (contiguous extents multiple of 8), batched with
+    both operands strided, leading dimensions wider than the matrices, and the
+    two-CTA short-K tiles / split-K up to eight waves the dispatcher picks."""
+    rng = np.random.default_rng(7 * m + n + 3 * k + opa + 2 * opb)
+    nb = 3
+    pad = 8  # ld = extent + 8: rows do not abut
+    ra, ca = (m, k) if opa == 0 else (k, m)
+    rb, cb = (k, n) if opb == 0 else (n, k)
+    a = crand(rng, nb, ra, ca + pad)
+    b = crand(rng, nb, rb, cb + pad)
+    c0 = crand(rng, nb, m, n)
+    ta, tb, tc = ctx.tensor(a), ctx.tensor(b), ctx.tensor(c0)
+    zgemm(ctx, opa, opb, m, n, k, ta.ptr, ca + pad, tb.ptr, cb + pad, tc.ptr, n, alpha=0.5, beta=-1.0, batch=nb,
+          stride_a=ra * (ca + pad), stride_b=rb * (cb + pad), stride_c=m * n)
+    ref = np.stack([0.5 * op(a[i, :, :ca], opa) @ op(b[i, :, :cb], opb) - c0[i] for i in range(nb)])
+    assert rel(tc.numpy(), ref) < 1e-13
