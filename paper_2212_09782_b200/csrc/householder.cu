@@ -751,9 +751,15 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
     // published as columns [J, J + w) of Y^H
     QT_CUDA(cudaStreamWaitEvent(sa, e.event(ev0 + 4 * b), 0));
     apply_block_reflector(Vb, kp, Tb, c + J * nc, nc, m - J, nc, static_cast<int>(w), CW, CW2, gs2, sa,
-                          [&] { extract(J, w, sa); stamp("ext" + std::to_string(b), sa); }, OB, true);
+                          [&] {
+                            extract(J, w, sa);
+                            stamp("ext" + std::to_string(b), sa);
+                            // the Y^H chain needs only the published block, not
+                            // the rest of C: release it here
+                            QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b + 2), sa));
+                          },
+                          OB, true);
     stamp("th" + std::to_string(b), sa);
-    QT_CUDA(cudaEventRecord(e.event(ev0 + 4 * b + 2), sa));
     // ---- X look-ahead: the next block's columns on sx, the rest on sxw
     const long long ntr = k - (J + w);
     if (ntr > 0) {
@@ -773,11 +779,15 @@ void qr_pair_tall(Engine& e, double2* x, long long m, long long k, double2* c, l
     // ---- Y^H block b (side3): the finished blocks' combined reflector
     // (left-looking), its panels, its T_ob, and T_all's new block column
     QT_CUDA(cudaStreamWaitEvent(sy, e.event(ev0 + 4 * b + 2), 0));
+    stamp("Ys" + std::to_string(b), sy);
     if (b > 0)
       apply_block_reflector(Vy, kp, TALL, yh + J, k, nc, w, static_cast<int>(J), YW, YW2, gsy, sy, nullptr, k, true);
+    stamp("Yl" + std::to_string(b), sy);
     outer_block_factor(e, yh, k, nc, k, Vy, kp, Ty, J, w, YW, YW2, gsy, by, sy);
+    stamp("Yf" + std::to_string(b), sy);
     double2* Tyb = TOBy + b * OB * OB;
     outer_block_tob(e, Vy, kp, Ty, J, w, k, nc, Tyb, OB, Gy, Gy + static_cast<size_t>(OB) * OB, gsy, sy);
+    stamp("Yt" + std::to_string(b), sy);
     copy2d(e, Tyb, OB, TALL + J * k + J, k, w, w, sy);
     if (b > 0) {
       GemmDesc gg;  // V_prev^H V_b (J x w), rows J.. of both (V_prev is zero above its own rows < J only)
