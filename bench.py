@@ -438,6 +438,30 @@ def run_chain(args, cc, as_anchor=False):
     launches = ctx.lib.qt_kernel_launches() - launches0
     tot_ms = max_over_ranks(sum(step_ms), ws)
     ms_per_step = tot_ms / steps
+
+    # ---------------- e2e: this rank's block of the chain (site tensors and
+    # bond matrices) copied in from pinned host memory before and out after
+    # every step, through the same C-ABI calls
+    def state_views():
+        return [chain.view("site", m) for m in range(start, end)] + [chain.view("bond", m) for m in range(start, end)]
+
+    host_in = [torch.from_numpy(np.ascontiguousarray(v.numpy()).view(np.float64)).pin_memory() for v in state_views()]
+    host_out = [torch.empty_like(t).pin_memory() for t in host_in]
+    h2d = sum(t.numel() * 8 for t in host_in)
+    lib = ctx.lib
+    barrier(ws)
+    ctx.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(steps):
+        for t, hb in zip(state_views(), host_in):
+            _capi.check(lib.qt_tensor_upload_async(t.h, _capi.C.cast(hb.data_ptr(), _capi.DP)))
+        chain.step(layers, scheme, pol)
+        for t, hb in zip(state_views(), host_out):
+            _capi.check(lib.qt_tensor_download_async(t.h, _capi.C.cast(hb.data_ptr(), _capi.DP)))
+    f1.record(stream)
+    ctx.synchronize()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1), ws) / steps
     chis = chain_dims(n, d, chi)
     f_step = 0.0
     for parity, _ in layers:
@@ -455,6 +479,8 @@ def run_chain(args, cc, as_anchor=False):
                 "straddling site tensors" if ws > 1 else f"C-ABI qt_tebd_step_finite_sharded, {workers} worker contexts",
         "updates_per_s": upd_per_step * 1e3 / ms_per_step,
         "step_ms": [round(x, 3) for x in step_ms],
+        "e2e": {"value": 1e3 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": h2d * ws,
+                "scope": "each rank's site tensors and bond matrices from pinned host memory in and out every step"},
         "roofline": {"bound": "tensor", "achieved": f_step / (ms_per_step * 1e-3) / 1e12, "peak": dmma_peak * ws,
                      "unit": "TFLOP/s", "frac": f_step / (ms_per_step * 1e-3) / 1e12 / (dmma_peak * ws),
                      "traffic": None, "scope": "whole chain step (all kernels), algorithmic flops / device time",
