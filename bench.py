@@ -507,9 +507,29 @@ def run_chain_reference(args, cc):
     upper bound since edge bonds are cheaper."""
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
+    n, d, chi = cc["n"], cc["d"], cc["chi"]
+    upd = 2 * len(range(0, n - 1, 2)) + len(range(1, n - 1, 2))
+    # the reference itself (oracle/_ref/ref_bench) on a central chi x chi bond
+    # cell, when it is built: per-update time x updates per chain step
+    cell = (f"C5 central bond d={d}, chi={chi}", d, chi, cc["scheme"], cc["explicit"], (0, 0.0))
+    rb = reference_binary_rate(cell, budget_s=20.0, min_updates=3)
+    if rb is not None:
+        cell_rate, n_upd, secs, threads = rb
+        t_upd = secs / n_upd
+        rate = 1.0 / (upd * t_upd)
+        line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
+                "steps": int(n_upd), "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+                "config": chain_config_dict(cc, int(os.environ.get("WORLD_SIZE", "1"))),
+                "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": int(threads), "kind": "reference",
+                                 "sample": f"{int(n_upd)} updates of a central chi={chi} bond cell by the reference's "
+                                           f"own apply_gate (oracle/_ref/ref_bench, {secs:.1f} s), step = {upd} "
+                                           "updates x mean update time (upper bound: edge bonds are cheaper)"},
+                "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
     from oracle import qrtebd_oracle as ref
     from paper_2212_09782_b200 import model
-    n, d, chi = cc["n"], cc["d"], cc["chi"]
     rng = np.random.default_rng(0x51AB)
     bm = ref.random_right_isometry(rng, d, chi, chi)
     bn = ref.random_right_isometry(rng, d, chi, chi)
@@ -523,8 +543,6 @@ def run_chain_reference(args, cc):
     for _ in range(k):
         ref.apply_gate_qr(xi, bm, bn, u, pol)
     t_upd = (time.perf_counter() - t0) / k
-    upd = (n - 1) + (n // 2) - 0  # 2 even layers of ceil((n-1)/2) + 1 odd layer of floor((n-1)/2)
-    upd = 2 * len(range(0, n - 1, 2)) + len(range(1, n - 1, 2))
     rate = 1.0 / (upd * t_upd)
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
             "steps": k, "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "strong",
