@@ -31,6 +31,9 @@ with tempfile.TemporaryDirectory() as td:
     for name in ("ref_bench", "b200_bench"):
         exe = os.path.join(ROOT, "oracle", "_ref", name)
         env = dict(os.environ, OPENBLAS_NUM_THREADS=str(os.cpu_count() or 1))
+        if os.environ.get("DROPIN_MALLOC_TUNE"):
+            # keep large freed blocks in the heap (no munmap / re-fault of fresh pages per call)
+            env["GLIBC_TUNABLES"] = "glibc.malloc.mmap_threshold=4294967295:glibc.malloc.trim_threshold=68719476736"
         r = subprocess.run([exe, path, str(d), str(chi), scheme, "1" if explicit else "0", str(dabs), str(drel),
                             budget, "3"], capture_output=True, text=True, env=env)
         if r.returncode != 0:
